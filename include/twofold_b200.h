@@ -1,0 +1,163 @@
+/*
+ * twofold_b200.h — C ABI of the B200 (sm_100a) twofold summation / dot library.
+ *
+ * The reference (arXiv 1401.0248 package `twofold`, pure Python + numba) has no
+ * FFI: its hot-path boundary is the Python call
+ *     run_flavor(method, flavor, data, b=None) -> SumResult     (pkg/src/twofold/kernels.py:591-640)
+ * and the ten wrappers sum_* / dot_*                              (kernels.py:669-706).
+ * Every entry point below replaces one piece of that boundary; the mapping is
+ * given per function.  Python binds these with ctypes.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  Device pointers are CUDA device (or
+ *     managed) addresses; `stream` is a cudaStream_t passed as void*.
+ *   - No function allocates memory.  Scratch (leaf partials + retire
+ *     counters) is owned by the caller; size it with tf_workspace_size().
+ *     Counters must be zero on entry; every kernel leaves them zero.
+ *   - All launches are stream-ordered and asynchronous; nothing synchronizes.
+ *   - Return value: TF_OK (0) or a TF_E* code; tf_strerror() names it and
+ *     tf_last_cuda_error() gives the CUDA error text of the calling thread.
+ *   - Result pairs are (value, error) of the accumulator type: the data type,
+ *     except TF_WIDE (float32 data, float64 accumulator; kernels.py:135-140).
+ *     For TF_DIRECT / TF_WIDE the error slot is +0 (kernels.py:615-621).  For
+ *     TF_KAHAN it carries the pending compensation c so that pairs stay
+ *     mergeable across shards; the reference reports 0 there (kernels.py:627)
+ *     and so does the Python shim.
+ *   - Arithmetic is strict IEEE-754 round-to-nearest-even, no FMA contraction,
+ *     no flush-to-zero (kernels.py:17-21); dot products round the
+ *     product in the data precision before summing (kernels.py:23-26, :209).
+ */
+#ifndef TWOFOLD_B200_H
+#define TWOFOLD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The Python shim maps them to the reference's exception
+ * types: DTYPE -> TypeError (kernels.py:576-581, :600-601), SHAPE -> ValueError
+ * (kernels.py:582-583), CANARY -> RuntimeError (kernels.py:559-565). */
+#define TF_OK              0
+#define TF_EINVAL_METHOD   1  /* unknown method id                                  */
+#define TF_EINVAL_DTYPE    2  /* dtype not f32/f64, or WIDE on f64 data             */
+#define TF_EINVAL_SHAPE    3  /* negative length, rows/cols/leading dim mismatch    */
+#define TF_EINVAL_ARG      4  /* bad lane count / leaf size / distribution / null   */
+#define TF_EWORKSPACE      5  /* workspace missing or too small                     */
+#define TF_ECUDA           6  /* a CUDA runtime call failed (tf_last_cuda_error)    */
+#define TF_ECANARY         7  /* device strict-rounding canary failed               */
+
+/* Methods, in the order of twofold.kernels.Method (kernels.py:44-49). */
+#define TF_DIRECT            0  /* sum / dot            kernels.py:127-132, :186-191 */
+#define TF_WIDE              1  /* sumd / dotd          kernels.py:135-140, :194-200 */
+#define TF_TWOFOLD_FAST      2  /* sumtf / dottf        kernels.py:143-154, :203-214 */
+#define TF_TWOFOLD_RIGOROUS  3  /* sumt / dott          kernels.py:157-170, :217-230 */
+#define TF_KAHAN             4  /* sumk / dotk          kernels.py:173-183, :233-243 */
+
+/* Data types. */
+#define TF_F32 0
+#define TF_F64 1
+
+/* Distributions for tf_fill (BASELINE.json configs). */
+#define TF_DIST_UNIFORM01   0  /* [0,1):  f32 (u32>>8)*2^-24, f64 (u64>>11)*2^-53        */
+#define TF_DIST_UNIFORM_SYM 1  /* [-1,1): 2u-1, exact in T (lcg.py:58-59 convention)     */
+#define TF_DIST_NORMAL      2  /* N(0,1) Box-Muller in f64, rounded to T                   */
+#define TF_DIST_ILLCOND     3  /* cfg3: permuted +-U[p0,p0+p1) pairs + p2*U[0,1) half     */
+
+/* Library build identity (bumps when the reduction tree changes). */
+int tf_version(void);
+const char* tf_strerror(int code);
+/* Text of the last CUDA error seen by this thread ("" if none). */
+const char* tf_last_cuda_error(void);
+
+/* Device strict-rounding canary: runs the kernels' own EFT and dot-step code on
+ * runtime operands — fast_two_sum(1, 2^-53) must return (1, 2^-53) in f64 and
+ * (1, 2^-24) in f32, and fl(fl(a*b) + s) must differ from fma(a, b, s).
+ * Replaces the import-time canary kernels.py:545-568 (and eft.py:59-66).
+ * Synchronous (one tiny launch + copy on the legacy default stream). */
+int tf_canary(void);
+
+/* Auto leaf size (log2 elements) the grid reduction uses for an n-element row:
+ * clamp(ceil_log2(n) - 11, log2(256*V*8), 16) with V = 16/sizeof(T).
+ * A pure function of (dtype, n): results never depend on the SM count. */
+int tf_leaf_log2(int dtype, int64_t n);
+
+/* Scratch for rows x cols (1-D: rows = 1, cols = n) at leaf_log2 (0 = auto):
+ *   partials: rows * leaves(cols) (value, error) pairs, any contents on entry;
+ *   counters: `rows` uint32 retire-tickets, ZERO on entry and left zero on exit
+ *             (so a caller can keep one zeroed counter buffer per stream).
+ * Only needed when a row spans more than one leaf (*leaves > 1). */
+int tf_workspace_size(int method, int dtype, int64_t rows, int64_t cols, int leaf_log2,
+                      size_t* partials_bytes, int64_t* counters, int64_t* leaves);
+
+/* Grid reduction ("cuda" flavor) of one contiguous array: one fused launch
+ * (leaf partials -> last-CTA balanced tree).  y == NULL: sum of x; else dot.
+ * out_pair: device, 2 accumulator elements.  Replaces run_flavor(method, <any
+ * flavor>, x[, y]) (kernels.py:591-640) for the GPU flavor.  leaf_log2 = 0 picks
+ * tf_leaf_log2(dtype, n); pass the GLOBAL array's leaf size when x is one shard
+ * of a larger array so the shard's tree is a subtree of the whole. */
+int tf_reduce(int method, int dtype, const void* x, const void* y, int64_t n,
+              int leaf_log2, void* out_pair, void* partials, size_t partials_bytes,
+              void* counters, int64_t counters_len, void* stream);
+
+/* Batched row-wise reduction: rows x cols, row r at x + r*ldx (elements).
+ * out_pairs: device, rows pairs.  Row r's pair is bit-identical to
+ * tf_reduce(x + r*ldx, cols) with the same leaf_log2 (no reference analogue:
+ * equals a per-row loop of dot_twofold_fast). */
+int tf_reduce_rows(int method, int dtype, const void* x, const void* y,
+                   int64_t rows, int64_t cols, int64_t ldx, int64_t ldy,
+                   int leaf_log2, void* out_pairs, void* partials, size_t partials_bytes,
+                   void* counters, int64_t counters_len, void* stream);
+
+/* Leaf partials only (no tree): partials_out[0 .. ceil(n/2^leaf_log2)) for an
+ * n-element chunk whose first element starts a leaf.  Used for streamed
+ * host->device inputs and by the shard layer; finish with tf_merge_tree. */
+int tf_reduce_leaves(int method, int dtype, const void* x, const void* y, int64_t n,
+                     int leaf_log2, void* partials_out, void* stream);
+
+/* Balanced binary tree (padded to a power of two with (+0,+0)) over `count`
+ * device pairs, using the method's merge: TwoSum + error fold for twofold
+ * (kernels.py:310-317), Kahan feed (kernels.py:379-390), plain add otherwise.
+ * Used after the NCCL all-gather of per-rank pairs.  count == 0 gives (+0,+0). */
+int tf_merge_tree(int method, int dtype, const void* pairs, int64_t count,
+                  void* out_pair, void* stream);
+
+/* Sequential flavor on the GPU: one thread runs the reference recurrence left
+ * to right — bit-identical to the reference `seq` kernels (kernels.py:127-243). */
+int tf_reduce_seq(int method, int dtype, const void* x, const void* y, int64_t n,
+                  void* out_pair, void* stream);
+
+/* Lane flavor (unroll:k / vec:k) on the GPU: k lanes striding the array, merged
+ * left to right, tail continued on the merged state — bit-identical to the
+ * reference lane kernels (kernels.py:257-541).  lanes: power of two in [2,16]. */
+int tf_reduce_lanes(int method, int dtype, const void* x, const void* y, int64_t n,
+                    int lanes, void* out_pair, void* stream);
+
+/* Elementwise EFTs on device arrays: kind 0 = fast_two_sum (eft.py:28-42),
+ * kind 1 = two_sum (eft.py:45-56).  x_out = fl(a+b), y_out = round-off. */
+int tf_eft(int kind, int dtype, const void* a, const void* b, int64_t n,
+           void* x_out, void* y_out, void* stream);
+
+/* Seeded Philox4x32-10 fill: element i of the stream uses counter
+ * (offset+i, stream_id) and key = seed, so any shard [o, o+n) of a stream is
+ * generated independently of the shard layout.  p0..p2: distribution
+ * parameters (ILLCOND: p0 = 1e8, p1 = 9e8, p2 = 1e-3 for cfg3; total length
+ * for the permutation is p3_total). */
+int tf_fill(int dist, int dtype, uint64_t seed, uint64_t stream_id, uint64_t offset,
+            int64_t n, double p0, double p1, double p2, int64_t total,
+            void* out, void* stream);
+
+/* cfg4 rows: out[r*ld + c] = N(0,1)[stream_id, (row0+r)*cols + c] * 10^U_r with
+ * U_r = lo + (hi-lo)*u(seed, scale_stream, row0+r), one scale per row. */
+int tf_fill_rows_scaled(int dtype, uint64_t seed, uint64_t stream_id,
+                        uint64_t scale_stream, int64_t row0, int64_t rows,
+                        int64_t cols, int64_t ld, double lo, double hi,
+                        void* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TWOFOLD_B200_H */

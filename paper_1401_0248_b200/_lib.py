@@ -1,0 +1,102 @@
+"""ctypes binding of the in-tree C-ABI library libtwofold_b200.so.
+
+The library is the only compute path of this package: if it is missing or
+the device canary fails, every call raises — there is no CPU fallback.
+Status codes map to the reference's exception types (kernels.py:574-584,
+:600-601, :559-565): DTYPE -> TypeError, SHAPE/ARG/METHOD -> ValueError,
+CANARY/CUDA/WORKSPACE -> RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtwofold_b200.so")
+
+TF_OK = 0
+TF_EINVAL_METHOD, TF_EINVAL_DTYPE, TF_EINVAL_SHAPE, TF_EINVAL_ARG = 1, 2, 3, 4
+TF_EWORKSPACE, TF_ECUDA, TF_ECANARY = 5, 6, 7
+
+TF_F32, TF_F64 = 0, 1
+DIST_UNIFORM01, DIST_UNIFORM_SYM, DIST_NORMAL, DIST_ILLCOND = 0, 1, 2, 3
+
+_lock = threading.Lock()
+_lib = None
+_canary_ok: set[int] = set()
+
+
+def _bind(L):
+    vp, i64, i32, u64, sz, dbl = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64,
+                                  ctypes.c_size_t, ctypes.c_double)
+    sig = {
+        "tf_version": ([], i32),
+        "tf_strerror": ([i32], ctypes.c_char_p),
+        "tf_last_cuda_error": ([], ctypes.c_char_p),
+        "tf_canary": ([], i32),
+        "tf_leaf_log2": ([i32, i64], i32),
+        "tf_workspace_size": ([i32, i32, i64, i64, i32, ctypes.POINTER(sz), ctypes.POINTER(i64),
+                               ctypes.POINTER(i64)], i32),
+        "tf_reduce": ([i32, i32, vp, vp, i64, i32, vp, vp, sz, vp, i64, vp], i32),
+        "tf_reduce_rows": ([i32, i32, vp, vp, i64, i64, i64, i64, i32, vp, vp, sz, vp, i64, vp], i32),
+        "tf_reduce_leaves": ([i32, i32, vp, vp, i64, i32, vp, vp], i32),
+        "tf_merge_tree": ([i32, i32, vp, i64, vp, vp], i32),
+        "tf_reduce_seq": ([i32, i32, vp, vp, i64, vp, vp], i32),
+        "tf_reduce_lanes": ([i32, i32, vp, vp, i64, i32, vp, vp], i32),
+        "tf_eft": ([i32, i32, vp, vp, i64, vp, vp, vp], i32),
+        "tf_fill": ([i32, i32, u64, u64, u64, i64, dbl, dbl, dbl, i64, vp, vp], i32),
+        "tf_fill_rows_scaled": ([i32, u64, u64, u64, i64, i64, i64, i64, dbl, dbl, vp, vp], i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    return L
+
+
+def lib():
+    """Load the library (no GPU needed to load; compute calls need one)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise ImportError(
+                        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                        "g.build()'` (or make -C paper_1401_0248_b200/csrc); there is no CPU fallback")
+                _lib = _bind(ctypes.CDLL(LIB_PATH))
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc == TF_OK:
+        return
+    L = lib()
+    msg = L.tf_strerror(rc).decode()
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == TF_EINVAL_DTYPE:
+        raise TypeError(msg)
+    if rc in (TF_EINVAL_SHAPE, TF_EINVAL_ARG, TF_EINVAL_METHOD):
+        raise ValueError(msg)
+    if rc == TF_ECUDA:
+        raise RuntimeError(f"{msg} ({L.tf_last_cuda_error().decode()})")
+    raise RuntimeError(msg)
+
+
+def ensure_canary(device_index: int) -> None:
+    """Run the device strict-rounding canary once per device (kernels.py:559-568)."""
+    if device_index in _canary_ok:
+        return
+    import torch
+    with torch.cuda.device(device_index):
+        rc = lib().tf_canary()
+    if rc == TF_ECANARY:
+        raise RuntimeError(
+            "compiled kernels violate strict IEEE rounding (device canary: fast_two_sum(1, 2**-53) "
+            "lost its round-off or a product was fused into an FMA); the library is unusable for "
+            "error tracking")
+    check(rc, "tf_canary")
+    _canary_ok.add(device_index)

@@ -1,0 +1,247 @@
+// misc.cu — status strings, the device strict-rounding canary, elementwise
+// EFT kernels and the seeded Philox input generators.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+
+#include "eft.cuh"
+#include "philox.cuh"
+#include "status.h"
+#include "twofold_b200.h"
+
+namespace tfb {
+
+static thread_local char g_cuda_err[256] = {0};
+
+void set_cuda_error(cudaError_t e) {
+  std::snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e),
+                cudaGetErrorString(e));
+}
+
+// ---------------------------------------------------------------------------
+// Canary (replaces kernels.py:545-568).  Operands live in device memory so
+// nothing is constant-folded; the kernel runs the same step/merge templates
+// the reductions use.
+__device__ double g_canary_in[8];
+__device__ double g_canary_out[8];
+
+__global__ void canary_kernel() {
+  const double* in = g_canary_in;
+  double* out = g_canary_out;
+  double x, y;
+  fast_two_sum<double>(in[0], in[1], x, y);  // (1, 2^-53) -> (1, 2^-53)
+  out[0] = x;
+  out[1] = y;
+  float xf, yf;
+  fast_two_sum<float>(static_cast<float>(in[0]), static_cast<float>(in[2]), xf, yf);  // (1, 2^-24)
+  out[2] = xf;
+  out[3] = yf;
+  // fl(fl(a*b) + s) == 0 exactly; a contracted fma(a, b, s) would give 2^-60.
+  Pair<double> st{in[4], 0.0};
+  step<kFast, double>(st, addend<kFast, double, true>(in[3], in[3]));
+  out[4] = st.s;
+  // binary32 twin: a = 1 + 2^-13, s = -(1 + 2^-12); fma would give 2^-26.
+  Pair<float> sf{static_cast<float>(in[6]), 0.0f};
+  step<kRigorous, float>(sf, addend<kRigorous, float, true>(static_cast<float>(in[5]),
+                                                            static_cast<float>(in[5])));
+  out[5] = sf.s;
+  // twofold merge keeps the absorbed addend: (1,0) (+) (2^-53,0) -> (1, 2^-53)
+  Pair<double> m = merge<kFast, double>(Pair<double>{in[0], 0.0}, Pair<double>{in[1], 0.0});
+  out[6] = m.s;
+  out[7] = m.e;
+}
+
+// ---------------------------------------------------------------------------
+// Elementwise EFTs (eft.py:28-56).
+template <typename T>
+__global__ void eft_kernel(int kind, const T* __restrict__ a, const T* __restrict__ b, int64_t n,
+                           T* __restrict__ xo, T* __restrict__ yo) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    T x, y;
+    if (kind == 0) fast_two_sum<T>(a[i], b[i], x, y);
+    else two_sum<T>(a[i], b[i], x, y);
+    xo[i] = x;
+    yo[i] = y;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Generators.
+__device__ __forceinline__ double normal_at(uint64_t seed, uint64_t sid, uint64_t i) {
+  U4 r = philox_at(seed, sid, i);
+  const double u1 = u01_f64(r);     // [0,1)  ->  1-u1 in (0,1]
+  const double u2 = u01_f64_hi(r);
+  return sqrt(-2.0 * log(1.0 - u1)) * cospi(2.0 * u2);
+}
+
+template <typename T>
+__device__ __forceinline__ T uniform_at(uint64_t seed, uint64_t sid, uint64_t i);
+template <>
+__device__ __forceinline__ float uniform_at<float>(uint64_t seed, uint64_t sid, uint64_t i) {
+  return u01_f32(philox_at(seed, sid, i));
+}
+template <>
+__device__ __forceinline__ double uniform_at<double>(uint64_t seed, uint64_t sid, uint64_t i) {
+  return u01_f64(philox_at(seed, sid, i));
+}
+
+template <typename T>
+__global__ void fill_kernel(int dist, uint64_t seed, uint64_t sid, uint64_t offset, int64_t n,
+                            double p0, double p1, double p2, int64_t total, T* __restrict__ out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t p = offset + static_cast<uint64_t>(i);
+    T v;
+    if (dist == TF_DIST_UNIFORM01) {
+      v = uniform_at<T>(seed, sid, p);
+    } else if (dist == TF_DIST_UNIFORM_SYM) {
+      const T u = uniform_at<T>(seed, sid, p);
+      v = Ar<T>::sub(Ar<T>::mul(T(2), u), T(1));
+    } else if (dist == TF_DIST_NORMAL) {
+      v = static_cast<T>(normal_at(seed, sid, p));
+    } else {  // TF_DIST_ILLCOND (cfg3): keyed-permuted +-b_k pairs + small half
+      const uint64_t tot = static_cast<uint64_t>(total);
+      const uint64_t q = feistel_permute(p, tot, seed);
+      const uint64_t h = tot / 4;
+      double d;
+      if (q < 2 * h) {
+        const uint64_t k = q < h ? q : q - h;
+        const double b = __dadd_rn(p0, __dmul_rn(p1, u01_f64(philox_at(seed, sid, k))));
+        d = q < h ? b : -b;
+      } else {
+        d = __dmul_rn(p2, u01_f64(philox_at(seed, sid + 1, q)));
+      }
+      v = static_cast<T>(d);
+    }
+    out[i] = v;
+  }
+}
+
+template <typename T>
+__global__ void fill_rows_scaled_kernel(uint64_t seed, uint64_t sid, uint64_t scale_sid,
+                                        int64_t row0, int64_t rows, int64_t cols, int64_t ld,
+                                        double lo, double hi, T* __restrict__ out) {
+  const int64_t total = rows * cols;
+  for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = idx / cols;
+    const int64_t c = idx - r * cols;
+    const uint64_t grow = static_cast<uint64_t>(row0 + r);
+    const double z = normal_at(seed, sid, grow * static_cast<uint64_t>(cols) + c);
+    const double U = __dadd_rn(lo, __dmul_rn(__dsub_rn(hi, lo), u01_f64(philox_at(seed, scale_sid, grow))));
+    const double s = exp10(U);
+    out[r * ld + c] = static_cast<T>(__dmul_rn(z, s));
+  }
+}
+
+static unsigned grid_for(int64_t n, int threads) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t want = (n + threads - 1) / threads;
+  const int64_t cap = static_cast<int64_t>(sms) * 16;
+  if (want > cap) want = cap;
+  if (want < 1) want = 1;
+  return static_cast<unsigned>(want);
+}
+
+}  // namespace tfb
+
+using namespace tfb;
+
+extern "C" {
+
+int tf_version(void) { return 1; }
+
+const char* tf_strerror(int code) {
+  switch (code) {
+    case TF_OK: return "ok";
+    case TF_EINVAL_METHOD: return "unknown method";
+    case TF_EINVAL_DTYPE: return "unsupported dtype (float32/float64; wide needs float32)";
+    case TF_EINVAL_SHAPE: return "invalid shape (negative length or leading dimension < cols)";
+    case TF_EINVAL_ARG: return "invalid argument";
+    case TF_EWORKSPACE: return "workspace missing or too small";
+    case TF_ECUDA: return "CUDA runtime error";
+    case TF_ECANARY: return "device kernels violate strict IEEE rounding";
+    default: return "unknown status";
+  }
+}
+
+const char* tf_last_cuda_error(void) { return g_cuda_err; }
+
+int tf_canary(void) {
+  const double in[8] = {1.0, 0x1p-53, 0x1p-24, 1.0 + 0x1p-30, -(1.0 + 0x1p-29),
+                        1.0 + 0x1p-13, -(1.0 + 0x1p-12), 0.0};
+  if (cudaMemcpyToSymbol(g_canary_in, in, sizeof(in)) != cudaSuccess) return record_cuda_error();
+  canary_kernel<<<1, 1>>>();
+  if (int rc = check_launch()) return rc;
+  double out[8];
+  if (cudaMemcpyFromSymbol(out, g_canary_out, sizeof(out)) != cudaSuccess) return record_cuda_error();
+  const bool ok = out[0] == 1.0 && out[1] == 0x1p-53 && out[2] == 1.0 && out[3] == 0x1p-24 &&
+                  out[4] == 0.0 && out[5] == 0.0 && out[6] == 1.0 && out[7] == 0x1p-53;
+  return ok ? TF_OK : TF_ECANARY;
+}
+
+int tf_eft(int kind, int dtype, const void* a, const void* b, int64_t n, void* x_out, void* y_out,
+           void* stream) {
+  if (kind != 0 && kind != 1) return TF_EINVAL_ARG;
+  if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
+  if (n < 0) return TF_EINVAL_SHAPE;
+  if (n == 0) return TF_OK;
+  if (!a || !b || !x_out || !y_out) return TF_EINVAL_ARG;
+  auto s = static_cast<cudaStream_t>(stream);
+  const unsigned g = grid_for(n, 256);
+  if (dtype == TF_F32)
+    eft_kernel<float><<<g, 256, 0, s>>>(kind, static_cast<const float*>(a),
+                                        static_cast<const float*>(b), n,
+                                        static_cast<float*>(x_out), static_cast<float*>(y_out));
+  else
+    eft_kernel<double><<<g, 256, 0, s>>>(kind, static_cast<const double*>(a),
+                                         static_cast<const double*>(b), n,
+                                         static_cast<double*>(x_out), static_cast<double*>(y_out));
+  return check_launch();
+}
+
+int tf_fill(int dist, int dtype, uint64_t seed, uint64_t stream_id, uint64_t offset, int64_t n,
+            double p0, double p1, double p2, int64_t total, void* out, void* stream) {
+  if (dist < TF_DIST_UNIFORM01 || dist > TF_DIST_ILLCOND) return TF_EINVAL_ARG;
+  if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
+  if (n < 0) return TF_EINVAL_SHAPE;
+  if (n == 0) return TF_OK;
+  if (!out) return TF_EINVAL_ARG;
+  if (dist == TF_DIST_ILLCOND &&
+      (total <= 0 || offset + static_cast<uint64_t>(n) > static_cast<uint64_t>(total)))
+    return TF_EINVAL_SHAPE;
+  auto s = static_cast<cudaStream_t>(stream);
+  const unsigned g = grid_for(n, 256);
+  if (dtype == TF_F32)
+    fill_kernel<float><<<g, 256, 0, s>>>(dist, seed, stream_id, offset, n, p0, p1, p2, total,
+                                         static_cast<float*>(out));
+  else
+    fill_kernel<double><<<g, 256, 0, s>>>(dist, seed, stream_id, offset, n, p0, p1, p2, total,
+                                          static_cast<double*>(out));
+  return check_launch();
+}
+
+int tf_fill_rows_scaled(int dtype, uint64_t seed, uint64_t stream_id, uint64_t scale_stream,
+                        int64_t row0, int64_t rows, int64_t cols, int64_t ld, double lo, double hi,
+                        void* out, void* stream) {
+  if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
+  if (rows < 0 || cols < 0 || row0 < 0 || (rows > 1 && ld < cols)) return TF_EINVAL_SHAPE;
+  if (rows == 0 || cols == 0) return TF_OK;
+  if (!out) return TF_EINVAL_ARG;
+  auto s = static_cast<cudaStream_t>(stream);
+  const unsigned g = grid_for(rows * cols, 256);
+  if (dtype == TF_F32)
+    fill_rows_scaled_kernel<float><<<g, 256, 0, s>>>(seed, stream_id, scale_stream, row0, rows, cols,
+                                                     ld, lo, hi, static_cast<float*>(out));
+  else
+    fill_rows_scaled_kernel<double><<<g, 256, 0, s>>>(seed, stream_id, scale_stream, row0, rows,
+                                                      cols, ld, lo, hi, static_cast<double*>(out));
+  return check_launch();
+}
+
+}  // extern "C"

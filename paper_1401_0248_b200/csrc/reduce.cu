@@ -1,0 +1,620 @@
+// reduce.cu — sm_100a twofold reduction kernels and their C-ABI launchers.
+//
+// Reduction tree (the GPU's non-sequential flavor; DESIGN.md §3 states it and
+// oracle/twofold_oracle.c:tfo_emulate restates it bit-for-bit):
+//   leaf      L = 2^leaf_log2 contiguous elements, L = 256 * V * R
+//             (V = 16 B / sizeof(T) elements per vector, R vectors per thread)
+//   thread t  runs the reference's sequential recurrence over the leaf's
+//             elements start + (k*256 + t)*V + j, k = 0..R-1, j = 0..V-1
+//             (coalesced 16-byte loads; elements past n are skipped)
+//   leaf pair balanced contiguous binary tree over the 256 thread states
+//             (warp shuffles, then one shared-memory level)
+//   row pair  balanced contiguous binary tree over the row's leaf pairs,
+//             padded with (+0,+0) to a power of two, done by the CTA that
+//             retires the row's last leaf (atomic ticket; merge order is by
+//             leaf index, never by arrival order)
+// The partition depends only on (dtype, n, leaf_log2), so results are
+// bit-identical across reruns, grid sizes and SM counts.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include "eft.cuh"
+#include "twofold_b200.h"
+#include "status.h"
+
+namespace tfb {
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+template <typename T> struct Vec;
+template <> struct Vec<float> { using type = float4; static constexpr int V = 4; };
+template <> struct Vec<double> { using type = double2; static constexpr int V = 2; };
+
+// Streaming 128-bit loads: read-only path, no L1 allocation (each byte is
+// read exactly once).
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 r;
+  asm("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0,%1}, [%2];"
+      : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float vget(const float4& v, int j) {
+  return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ double vget(const double2& v, int j) { return j == 0 ? v.x : v.y; }
+
+template <typename A>
+__device__ __forceinline__ Pair<A> ld_pair_cg(const Pair<A>* p) {
+  Pair<A> r;
+  r.s = __ldcg(&p->s);
+  r.e = __ldcg(&p->e);
+  return r;
+}
+
+template <int M> struct HasErr { static constexpr bool value = (M == kFast || M == kRigorous || M == kKahan); };
+
+// Balanced contiguous binary tree over the first `width` (power of two,
+// 1..256) threads' states; result valid in thread 0.  Level `off` merges
+// thread t (t % 2off == 0) with thread t + off as the right operand.
+template <int M, typename A>
+__device__ __forceinline__ Pair<A> block_tree(Pair<A> st, Pair<A>* smem, int width) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int wl = width < 32 ? width : 32;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    if (off >= wl) break;
+    Pair<A> o;
+    o.s = __shfl_down_sync(0xffffffffu, st.s, off);
+    if constexpr (HasErr<M>::value) o.e = __shfl_down_sync(0xffffffffu, st.e, off);
+    else o.e = A(0);
+    if ((lane & (2 * off - 1)) == 0) st = merge<M, A>(st, o);
+  }
+  if (width > 32) {
+    if (lane == 0) smem[warp] = st;
+    __syncthreads();
+    if (warp == 0) {
+      const int nw = width >> 5;
+      st = lane < nw ? smem[lane] : zero_pair<A>();
+#pragma unroll
+      for (int off = 1; off < kWarps; off <<= 1) {
+        if (off >= nw) break;
+        Pair<A> o;
+        o.s = __shfl_down_sync(0xffffffffu, st.s, off);
+        if constexpr (HasErr<M>::value) o.e = __shfl_down_sync(0xffffffffu, st.e, off);
+        else o.e = A(0);
+        if ((lane & (2 * off - 1)) == 0) st = merge<M, A>(st, o);
+      }
+    }
+    __syncthreads();
+  }
+  return st;
+}
+
+// Balanced tree over P pairs (padded with (+0,+0) to P2 = pow2ceil(P)) by one
+// CTA.  If P2 >= 256, thread t first folds leaves [t*g, (t+1)*g), g = P2/256,
+// with a binary-counter stack (the same balanced shape, sequentially), then
+// the 256-thread tree finishes; otherwise threads < P2 hold one pair each.
+template <int M, typename A>
+__device__ Pair<A> tree_over(const Pair<A>* parts, int64_t P, Pair<A>* smem) {
+  int64_t P2 = 1;
+  while (P2 < P) P2 <<= 1;
+  const int t = threadIdx.x;
+  if (P2 >= kThreads) {
+    const int64_t g = P2 / kThreads;
+    const int64_t base = static_cast<int64_t>(t) * g;
+    Pair<A> stack[32];
+    for (int64_t i0 = 0; i0 < g; i0 += 8) {
+      Pair<A> buf[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int64_t idx = base + i0 + q;
+        buf[q] = (i0 + q < g && idx < P) ? ld_pair_cg(parts + idx) : zero_pair<A>();
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int64_t i = i0 + q;
+        if (i < g) {
+          Pair<A> cur = buf[q];
+          int b = 0;
+          for (; (i >> b) & 1; ++b) cur = merge<M, A>(stack[b], cur);
+          stack[b] = cur;
+        }
+      }
+    }
+    int lg = 0;
+    while ((int64_t(1) << lg) < g) ++lg;
+    return block_tree<M, A>(stack[lg], smem, kThreads);
+  }
+  Pair<A> cur = t < P ? ld_pair_cg(parts + t) : zero_pair<A>();
+  return block_tree<M, A>(cur, smem, static_cast<int>(P2));
+}
+
+// One thread's sequential recurrence over its elements of the leaf at
+// `start` of a row of n elements.  VEC: 16-byte aligned row, full leaf.
+template <int M, typename T, bool DOT, bool VEC, int U>
+__device__ __forceinline__ Pair<typename Acc<M, T>::type> leaf_chain(
+    const T* __restrict__ x, const T* __restrict__ y, int64_t start, int64_t n, int R) {
+  using A = typename Acc<M, T>::type;
+  using VT = typename Vec<T>::type;
+  constexpr int V = Vec<T>::V;
+  Pair<A> st = zero_pair<A>();
+  const int t = threadIdx.x;
+  const int64_t L = static_cast<int64_t>(R) * kThreads * V;
+  if (VEC && start + L <= n) {
+    const VT* xv = reinterpret_cast<const VT*>(x + start) + t;
+    const VT* yv = DOT ? reinterpret_cast<const VT*>(y + start) + t : nullptr;
+    int k = 0;
+    for (; k + U <= R; k += U) {
+      VT a[U], b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a[u] = ld_stream(xv + static_cast<int64_t>(k + u) * kThreads);
+        if constexpr (DOT) b[u] = ld_stream(yv + static_cast<int64_t>(k + u) * kThreads);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          if constexpr (DOT) step<M, A>(st, addend<M, T, true>(vget(a[u], j), vget(b[u], j)));
+          else step<M, A>(st, addend<M, T, false>(vget(a[u], j), T(0)));
+        }
+      }
+    }
+    for (; k < R; ++k) {
+      VT a = ld_stream(xv + static_cast<int64_t>(k) * kThreads);
+      VT b;
+      if constexpr (DOT) b = ld_stream(yv + static_cast<int64_t>(k) * kThreads);
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        if constexpr (DOT) step<M, A>(st, addend<M, T, true>(vget(a, j), vget(b, j)));
+        else step<M, A>(st, addend<M, T, false>(vget(a, j), T(0)));
+      }
+    }
+  } else {
+    for (int k = 0; k < R; ++k) {
+      const int64_t base = start + (static_cast<int64_t>(k) * kThreads + t) * V;
+      if (base >= n) break;  // later k only go further right
+#pragma unroll
+      for (int j = 0; j < V; ++j) {
+        const int64_t i = base + j;
+        if (i < n) {
+          if constexpr (DOT) step<M, A>(st, addend<M, T, true>(x[i], y[i]));
+          else step<M, A>(st, addend<M, T, false>(x[i], T(0)));
+        }
+      }
+    }
+  }
+  return st;
+}
+
+template <typename T> struct Unroll { static constexpr int value = 4; };
+
+// Grid reduction over rows x cols.  Unit u = (row r, leaf l), u = r*P + l.
+// mode 0: write leaf pairs to partials[u] only.  mode 1: fused — the CTA that
+// retires a row's last leaf builds the row tree into out[r].
+template <int M, typename T, bool DOT, bool VEC>
+__global__ void __launch_bounds__(kThreads) leaves_kernel(
+    const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy,
+    int64_t rows, int64_t cols, int leaf_log2, int64_t P,
+    Pair<typename Acc<M, T>::type>* __restrict__ partials, unsigned* __restrict__ counters,
+    Pair<typename Acc<M, T>::type>* __restrict__ out, int fused) {
+  using A = typename Acc<M, T>::type;
+  constexpr int V = Vec<T>::V;
+  __shared__ Pair<A> smem[kWarps];
+  __shared__ int s_last;
+  const int R = (1 << leaf_log2) / (kThreads * V);
+  const int64_t units = rows * P;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int64_t r = u / P;
+    const int64_t l = u - r * P;
+    const T* xr = x + r * ldx;
+    const T* yr = DOT ? y + r * ldy : nullptr;
+    Pair<A> st = leaf_chain<M, T, DOT, VEC, Unroll<T>::value>(
+        xr, yr, l << leaf_log2, cols, R);
+    st = block_tree<M, A>(st, smem, kThreads);
+    if (!fused) {
+      if (threadIdx.x == 0) partials[u] = st;
+      continue;
+    }
+    if (P == 1) {
+      if (threadIdx.x == 0) out[r] = st;
+      continue;
+    }
+    if (threadIdx.x == 0) {
+      partials[u] = st;
+      __threadfence();
+      const unsigned prev = atomicAdd(&counters[r], 1u);
+      s_last = (prev == static_cast<unsigned>(P - 1));
+    }
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      Pair<A> root = tree_over<M, A>(partials + r * P, P, smem);
+      if (threadIdx.x == 0) {
+        out[r] = root;
+        counters[r] = 0u;  // leave the workspace reusable
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int M, typename A>
+__global__ void __launch_bounds__(kThreads) tree_kernel(const Pair<A>* __restrict__ pairs,
+                                                        int64_t count, Pair<A>* __restrict__ out) {
+  __shared__ Pair<A> smem[kWarps];
+  Pair<A> root = count > 0 ? tree_over<M, A>(pairs, count, smem) : zero_pair<A>();
+  if (threadIdx.x == 0) out[0] = root;
+}
+
+// Sequential flavor: the reference recurrence, one thread, left to right.
+template <int M, typename T, bool DOT>
+__global__ void seq_kernel(const T* __restrict__ x, const T* __restrict__ y, int64_t n,
+                           Pair<typename Acc<M, T>::type>* __restrict__ out) {
+  using A = typename Acc<M, T>::type;
+  Pair<A> st = zero_pair<A>();
+  int64_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    T a[8], b[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      a[q] = x[i + q];
+      if constexpr (DOT) b[q] = y[i + q];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if constexpr (DOT) step<M, A>(st, addend<M, T, true>(a[q], b[q]));
+      else step<M, A>(st, addend<M, T, false>(a[q], T(0)));
+    }
+  }
+  for (; i < n; ++i) {
+    if constexpr (DOT) step<M, A>(st, addend<M, T, true>(x[i], y[i]));
+    else step<M, A>(st, addend<M, T, false>(x[i], T(0)));
+  }
+  out[0] = st;
+}
+
+// Lane flavor (kernels.py:257-541): lane j takes elements i*k + j of the
+// blocked prefix, lanes merge left to right, the tail n % k continues on the
+// merged state.
+template <int M, typename T, bool DOT>
+__global__ void lanes_kernel(const T* __restrict__ x, const T* __restrict__ y, int64_t n, int k,
+                             Pair<typename Acc<M, T>::type>* __restrict__ out) {
+  using A = typename Acc<M, T>::type;
+  __shared__ Pair<A> lane_state[16];
+  const int j = threadIdx.x;
+  const int64_t nb = n - n % k;
+  Pair<A> st = zero_pair<A>();
+  for (int64_t i = 0; i < nb; i += k) {
+    if constexpr (DOT) step<M, A>(st, addend<M, T, true>(x[i + j], y[i + j]));
+    else step<M, A>(st, addend<M, T, false>(x[i + j], T(0)));
+  }
+  lane_state[j] = st;
+  __syncthreads();
+  if (j != 0) return;
+  Pair<A> s;
+  if constexpr (M == kDirect || M == kWide) {
+    s = zero_pair<A>();  // s = 0; s = s + acc[j] for all j   (kernels.py:267-269)
+    for (int q = 0; q < k; ++q) s.s = Ar<A>::add(s.s, lane_state[q].s);
+  } else {
+    s = lane_state[0];
+    for (int q = 1; q < k; ++q) s = merge<M, A>(s, lane_state[q]);
+  }
+  for (int64_t i = nb; i < n; ++i) {
+    if constexpr (DOT) step<M, A>(s, addend<M, T, true>(x[i], y[i]));
+    else step<M, A>(s, addend<M, T, false>(x[i], T(0)));
+  }
+  out[0] = s;
+}
+
+// ---------------------------------------------------------------------------
+// Host side.
+
+struct DevInfo { int sms = 0; };
+
+static int device_sms() {
+  static std::mutex mu;
+  static std::unordered_map<int, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cache[dev] = sms;
+  return sms;
+}
+
+static int occupancy_of(const void* fn) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(fn);
+  if (it != cache.end()) return it->second;
+  int blocks = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kThreads, 0) != cudaSuccess ||
+      blocks < 1)
+    blocks = 1;
+  cache[fn] = blocks;
+  return blocks;
+}
+
+static inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int ceil_log2_i64(int64_t n) {
+  int l = 0;
+  while ((int64_t(1) << l) < n) ++l;
+  return l;
+}
+
+int min_leaf_log2(int dtype) {
+  // log2(256 threads * V * 8 vectors): 8192 f32 / 4096 f64 elements
+  return dtype == TF_F32 ? 13 : 12;
+}
+int floor_leaf_log2(int dtype) {  // smallest legal explicit leaf: one vector per thread
+  return dtype == TF_F32 ? 10 : 9;
+}
+
+int auto_leaf_log2(int dtype, int64_t n) {
+  int l = ceil_log2_i64(n > 0 ? n : 1) - 11;
+  const int lo = min_leaf_log2(dtype);
+  if (l < lo) l = lo;
+  if (l > 16) l = 16;
+  return l;
+}
+
+template <int M, typename T, bool DOT>
+static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy, int64_t rows,
+                         int64_t cols, int leaf_log2, void* partials, void* counters, void* out,
+                         int fused, cudaStream_t stream) {
+  using A = typename Acc<M, T>::type;
+  const int64_t P = (cols + (int64_t(1) << leaf_log2) - 1) >> leaf_log2;
+  const int64_t units = rows * P;
+  if (units == 0) return TF_OK;
+  const bool vec = aligned16(x) && ((ldx * int64_t(sizeof(T))) % 16 == 0 || rows == 1) &&
+                   (!DOT || (aligned16(y) && ((ldy * int64_t(sizeof(T))) % 16 == 0 || rows == 1)));
+  const void* fn = vec ? reinterpret_cast<const void*>(&leaves_kernel<M, T, DOT, true>)
+                       : reinterpret_cast<const void*>(&leaves_kernel<M, T, DOT, false>);
+  const int64_t slots = static_cast<int64_t>(device_sms()) * occupancy_of(fn);
+  const int64_t grid64 = units < slots ? units : slots;
+  const unsigned grid = static_cast<unsigned>(grid64 > 0 ? grid64 : 1);
+  auto px = static_cast<const T*>(x);
+  auto py = static_cast<const T*>(y);
+  auto pp = static_cast<Pair<A>*>(partials);
+  auto pc = static_cast<unsigned*>(counters);
+  auto po = static_cast<Pair<A>*>(out);
+  if (vec)
+    leaves_kernel<M, T, DOT, true><<<grid, kThreads, 0, stream>>>(px, py, ldx, ldy, rows, cols,
+                                                                   leaf_log2, P, pp, pc, po, fused);
+  else
+    leaves_kernel<M, T, DOT, false><<<grid, kThreads, 0, stream>>>(px, py, ldx, ldy, rows, cols,
+                                                                    leaf_log2, P, pp, pc, po, fused);
+  return check_launch();
+}
+
+template <int M, typename T, bool DOT>
+static int launch_seq(const void* x, const void* y, int64_t n, void* out, cudaStream_t s) {
+  using A = typename Acc<M, T>::type;
+  seq_kernel<M, T, DOT><<<1, 1, 0, s>>>(static_cast<const T*>(x), static_cast<const T*>(y), n,
+                                        static_cast<Pair<A>*>(out));
+  return check_launch();
+}
+
+template <int M, typename T, bool DOT>
+static int launch_lanes(const void* x, const void* y, int64_t n, int k, void* out, cudaStream_t s) {
+  using A = typename Acc<M, T>::type;
+  lanes_kernel<M, T, DOT><<<1, k, 0, s>>>(static_cast<const T*>(x), static_cast<const T*>(y), n, k,
+                                          static_cast<Pair<A>*>(out));
+  return check_launch();
+}
+
+template <int M, typename A>
+static int launch_tree(const void* pairs, int64_t count, void* out, cudaStream_t s) {
+  tree_kernel<M, A><<<1, kThreads, 0, s>>>(static_cast<const Pair<A>*>(pairs), count,
+                                           static_cast<Pair<A>*>(out));
+  return check_launch();
+}
+
+// Method x dtype x {sum, dot} dispatch.  WIDE exists for f32 data only
+// (kernels.py:600-601).
+#define TFB_DISPATCH(method, dtype, dot, CALL)                                   \
+  do {                                                                           \
+    if ((dtype) != TF_F32 && (dtype) != TF_F64) return TF_EINVAL_DTYPE;          \
+    if ((method) == TF_WIDE && (dtype) != TF_F32) return TF_EINVAL_DTYPE;        \
+    switch (method) {                                                            \
+      case TF_DIRECT:                                                            \
+        if ((dtype) == TF_F32) { if (dot) return CALL(kDirect, float, true);     \
+                                 else return CALL(kDirect, float, false); }      \
+        else { if (dot) return CALL(kDirect, double, true);                      \
+               else return CALL(kDirect, double, false); }                       \
+      case TF_WIDE:                                                              \
+        if (dot) return CALL(kWide, float, true);                                \
+        else return CALL(kWide, float, false);                                   \
+      case TF_TWOFOLD_FAST:                                                      \
+        if ((dtype) == TF_F32) { if (dot) return CALL(kFast, float, true);       \
+                                 else return CALL(kFast, float, false); }        \
+        else { if (dot) return CALL(kFast, double, true);                        \
+               else return CALL(kFast, double, false); }                         \
+      case TF_TWOFOLD_RIGOROUS:                                                  \
+        if ((dtype) == TF_F32) { if (dot) return CALL(kRigorous, float, true);   \
+                                 else return CALL(kRigorous, float, false); }    \
+        else { if (dot) return CALL(kRigorous, double, true);                    \
+               else return CALL(kRigorous, double, false); }                     \
+      case TF_KAHAN:                                                             \
+        if ((dtype) == TF_F32) { if (dot) return CALL(kKahan, float, true);      \
+                                 else return CALL(kKahan, float, false); }       \
+        else { if (dot) return CALL(kKahan, double, true);                       \
+               else return CALL(kKahan, double, false); }                        \
+      default:                                                                   \
+        return TF_EINVAL_METHOD;                                                 \
+    }                                                                            \
+  } while (0)
+
+static size_t pair_bytes(int method, int dtype) {
+  return (method == TF_WIDE || dtype == TF_F64) ? 16u : 8u;
+}
+
+static int validate(int method, int dtype) {
+  if (method < TF_DIRECT || method > TF_KAHAN) return TF_EINVAL_METHOD;
+  if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
+  if (method == TF_WIDE && dtype != TF_F32) return TF_EINVAL_DTYPE;
+  return TF_OK;
+}
+
+static int resolve_leaf(int dtype, int64_t cols, int leaf_log2, int* out) {
+  if (leaf_log2 == 0) {
+    *out = auto_leaf_log2(dtype, cols);
+    return TF_OK;
+  }
+  if (leaf_log2 < floor_leaf_log2(dtype) || leaf_log2 > 24) return TF_EINVAL_ARG;
+  *out = leaf_log2;
+  return TF_OK;
+}
+
+}  // namespace tfb
+
+using namespace tfb;
+
+extern "C" {
+
+int tf_leaf_log2(int dtype, int64_t n) {
+  if (dtype != TF_F32 && dtype != TF_F64) return -TF_EINVAL_DTYPE;
+  return auto_leaf_log2(dtype, n);
+}
+
+int tf_workspace_size(int method, int dtype, int64_t rows, int64_t cols, int leaf_log2,
+                      size_t* partials_bytes, int64_t* counters, int64_t* leaves) {
+  int rc = validate(method, dtype);
+  if (rc) return rc;
+  if (rows < 0 || cols < 0) return TF_EINVAL_SHAPE;
+  int lg;
+  if ((rc = resolve_leaf(dtype, cols, leaf_log2, &lg))) return rc;
+  const int64_t P = (cols + (int64_t(1) << lg) - 1) >> lg;
+  if (partials_bytes) *partials_bytes = static_cast<size_t>(rows * P) * pair_bytes(method, dtype);
+  if (counters) *counters = rows;
+  if (leaves) *leaves = P;
+  return TF_OK;
+}
+
+int tf_reduce_rows(int method, int dtype, const void* x, const void* y, int64_t rows, int64_t cols,
+                   int64_t ldx, int64_t ldy, int leaf_log2, void* out_pairs, void* partials,
+                   size_t partials_bytes, void* counters, int64_t counters_len, void* stream) {
+  int rc = validate(method, dtype);
+  if (rc) return rc;
+  if (rows < 0 || cols < 0) return TF_EINVAL_SHAPE;
+  if (rows > 1 && (ldx < cols || (y && ldy < cols))) return TF_EINVAL_SHAPE;
+  if (rows == 0) return TF_OK;
+  if (!out_pairs || (cols > 0 && !x)) return TF_EINVAL_ARG;
+  int lg;
+  if ((rc = resolve_leaf(dtype, cols, leaf_log2, &lg))) return rc;
+  auto s = static_cast<cudaStream_t>(stream);
+  if (cols == 0) {  // every row is empty: (+0, +0)
+    if (cudaMemsetAsync(out_pairs, 0, static_cast<size_t>(rows) * pair_bytes(method, dtype), s) !=
+        cudaSuccess)
+      return record_cuda_error();
+    return TF_OK;
+  }
+  size_t need = 0;
+  int64_t P = 0;
+  tf_workspace_size(method, dtype, rows, cols, lg, &need, nullptr, &P);
+  if (P > 1 && (!partials || partials_bytes < need || !counters || counters_len < rows))
+    return TF_EWORKSPACE;
+  void* parts = partials;
+  const bool dot = y != nullptr;
+#define TFB_CALL_LEAVES(M, T, DOT) \
+  launch_leaves<M, T, DOT>(x, y, ldx, ldy, rows, cols, lg, parts, counters, out_pairs, 1, s)
+  TFB_DISPATCH(method, dtype, dot, TFB_CALL_LEAVES);
+#undef TFB_CALL_LEAVES
+}
+
+int tf_reduce(int method, int dtype, const void* x, const void* y, int64_t n, int leaf_log2,
+              void* out_pair, void* partials, size_t partials_bytes, void* counters,
+              int64_t counters_len, void* stream) {
+  if (n < 0) return TF_EINVAL_SHAPE;
+  return tf_reduce_rows(method, dtype, x, y, 1, n, n, n, leaf_log2, out_pair, partials,
+                        partials_bytes, counters, counters_len, stream);
+}
+
+int tf_reduce_leaves(int method, int dtype, const void* x, const void* y, int64_t n, int leaf_log2,
+                     void* partials_out, void* stream) {
+  int rc = validate(method, dtype);
+  if (rc) return rc;
+  if (n < 0) return TF_EINVAL_SHAPE;
+  if (n == 0) return TF_OK;
+  if (!x || !partials_out) return TF_EINVAL_ARG;
+  int lg;
+  if ((rc = resolve_leaf(dtype, n, leaf_log2, &lg))) return rc;
+  auto s = static_cast<cudaStream_t>(stream);
+  const bool dot = y != nullptr;
+#define TFB_CALL_PARTS(M, T, DOT) \
+  launch_leaves<M, T, DOT>(x, y, n, n, 1, n, lg, partials_out, nullptr, nullptr, 0, s)
+  TFB_DISPATCH(method, dtype, dot, TFB_CALL_PARTS);
+#undef TFB_CALL_PARTS
+}
+
+int tf_merge_tree(int method, int dtype, const void* pairs, int64_t count, void* out_pair,
+                  void* stream) {
+  int rc = validate(method, dtype);
+  if (rc) return rc;
+  if (count < 0) return TF_EINVAL_SHAPE;
+  if (!out_pair || (count > 0 && !pairs)) return TF_EINVAL_ARG;
+  auto s = static_cast<cudaStream_t>(stream);
+  switch (method) {
+    case TF_DIRECT:
+      return dtype == TF_F32 ? launch_tree<kDirect, float>(pairs, count, out_pair, s)
+                             : launch_tree<kDirect, double>(pairs, count, out_pair, s);
+    case TF_WIDE:
+      return launch_tree<kWide, double>(pairs, count, out_pair, s);
+    case TF_TWOFOLD_FAST:
+      return dtype == TF_F32 ? launch_tree<kFast, float>(pairs, count, out_pair, s)
+                             : launch_tree<kFast, double>(pairs, count, out_pair, s);
+    case TF_TWOFOLD_RIGOROUS:
+      return dtype == TF_F32 ? launch_tree<kRigorous, float>(pairs, count, out_pair, s)
+                             : launch_tree<kRigorous, double>(pairs, count, out_pair, s);
+    default:
+      return dtype == TF_F32 ? launch_tree<kKahan, float>(pairs, count, out_pair, s)
+                             : launch_tree<kKahan, double>(pairs, count, out_pair, s);
+  }
+}
+
+int tf_reduce_seq(int method, int dtype, const void* x, const void* y, int64_t n, void* out_pair,
+                  void* stream) {
+  int rc = validate(method, dtype);
+  if (rc) return rc;
+  if (n < 0) return TF_EINVAL_SHAPE;
+  if (!out_pair || (n > 0 && !x)) return TF_EINVAL_ARG;
+  auto s = static_cast<cudaStream_t>(stream);
+  const bool dot = y != nullptr;
+#define TFB_CALL_SEQ(M, T, DOT) launch_seq<M, T, DOT>(x, y, n, out_pair, s)
+  TFB_DISPATCH(method, dtype, dot, TFB_CALL_SEQ);
+#undef TFB_CALL_SEQ
+}
+
+int tf_reduce_lanes(int method, int dtype, const void* x, const void* y, int64_t n, int lanes,
+                    void* out_pair, void* stream) {
+  int rc = validate(method, dtype);
+  if (rc) return rc;
+  if (n < 0) return TF_EINVAL_SHAPE;
+  if (lanes < 2 || lanes > 16 || (lanes & (lanes - 1))) return TF_EINVAL_ARG;
+  if (!out_pair || (n > 0 && !x)) return TF_EINVAL_ARG;
+  auto s = static_cast<cudaStream_t>(stream);
+  const bool dot = y != nullptr;
+#define TFB_CALL_LANES(M, T, DOT) launch_lanes<M, T, DOT>(x, y, n, lanes, out_pair, s)
+  TFB_DISPATCH(method, dtype, dot, TFB_CALL_LANES);
+#undef TFB_CALL_LANES
+}
+
+}  // extern "C"
