@@ -1,0 +1,454 @@
+"""Benchmark: twofold sum/dot throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg5]
+
+Default workload (BASELINE.json configs[4], the config the metric's
+"1/2/4/8 B200" is quoted on): fp64 twofold-fast dot (dottf) of U[-1,1)
+Philox streams (seed 4), 2^29 elements per rank, rank r owning elements
+[r*2^29, (r+1)*2^29) of the 2^32-element cfg5 stream, so N=8 is cfg5 in full
+and per-GPU work is fixed (weak scaling).  A step = one pass of the hot path
+over the rank's shard: the fused leaf+tree kernel, and for N>1 the NCCL
+all-gather of the 16-byte (v, e) pairs plus the merge kernel.  Inputs
+(8.6 GB per rank) are 68x the L2, so no flush is needed; the small configs
+(--config cfg1/cfg2/cfg2-small) flush L2 between steps.
+
+One JSON line on rank 0: value = elements/s over all ranks (device-timed,
+CUDA events, max over ranks), e2e = the same through the public API from
+pinned host buffers (H2D + reduce + D2H of the pair each step), roofline of
+the reduction kernel, cpu_baseline = the oracle's multi-thread port of the
+reference recurrence on this host.  --impl reference times that CPU port
+alone (rank 0), the reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "twofold sum/dot Gelem/s & HBM GB/s vs roofline at 1/2/4/8 B200, fp32/fp64"
+UNIT = "Gelem/s"
+PER_RANK = 1 << 29
+
+WORKLOADS = {
+    # name: (config key, method, per-rank elements or None = whole config, needs L2 flush)
+    "cfg5": ("cfg5", "twofold-fast", PER_RANK, False),
+    "cfg1": ("cfg1", "twofold-fast", None, True),
+    "cfg2": ("cfg2", "twofold-fast", None, True),
+    "cfg2-dott": ("cfg2", "twofold-rigorous", None, True),
+    "cfg2-small": ("cfg2-small", "twofold-fast", None, True),
+    "cfg3": ("cfg3", "twofold-rigorous", None, False),
+    "cfg3-sumk": ("cfg3", "kahan", None, False),
+    "cfg4": ("cfg4", "twofold-fast", None, False),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg5", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--leaf-log2", type=int, default=0, help="override the auto leaf size (sweeps)")
+    ap.add_argument("--graph", action="store_true", help="replay the timed steps from a CUDA graph")
+    return ap.parse_args()
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def workload_desc(name, cfg, method, n_rank, world):
+    from paper_1401_0248_b200.gen import CONFIGS  # noqa: F401
+    d = {
+        "workload": (f"{name}: {cfg.note}; {method} on {n_rank} elements per rank"
+                     + (f" (rank r owns [r*2^29,(r+1)*2^29) of the 2^32 stream; N=8 is cfg5 in full)"
+                        if name == "cfg5" else "")),
+        "op": cfg.op, "method": method, "n_per_rank": n_rank, "n_global": n_rank * world,
+        "data_dtype": "f64" if str(cfg.dtype).endswith("64") else "f32",
+        "generator": f"Philox4x32-10 seed {cfg.seed} (x stream 0, y stream 1)",
+        "parallelism": (f"dp{world}: contiguous shards + NCCL all-gather of (v,e) pairs"
+                        if world > 1 else "single GPU"),
+    }
+    return d
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks and throttle reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons = [], 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # NVML missing: report nothing rather than guess
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def report(self):
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+def measured_peak():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_for(name):
+    path = os.path.join(REPO, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(name)
+    except Exception:
+        return None
+
+
+def cpu_port_rate(method_id, xh, yh, nthreads, budget_s=12.0):
+    """Time the oracle's port of the reference recurrence (contiguous shards x seq + lane merge)."""
+    from oracle import oracle as O
+    n = xh.shape[0]
+    times = []
+    t_start = time.perf_counter()
+    res = None
+    while len(times) < 5 and (not times or time.perf_counter() - t_start < budget_s):
+        t0 = time.perf_counter()
+        res = O.threads(method_id, xh, yh, nthreads)
+        times.append(time.perf_counter() - t0)
+    best = min(times)
+    return n / best / 1e9, best, times, res
+
+
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    sys.path.insert(0, REPO)
+    from oracle import oracle as O
+    cfg_key, method, n_rank, _ = WORKLOADS[args.config]
+    import torch  # noqa: F401  (only for dtype names in the config)
+    from paper_1401_0248_b200.gen import CONFIGS
+    cfg = CONFIGS[cfg_key]
+    mid = O.METHODS.index(method)
+    nt = host_threads()
+    dt = np.float64 if str(cfg.dtype).endswith("64") else np.float32
+    n = n_rank or cfg.n
+    if cfg.dist in ("uniform01", "uniform_sym"):
+        xh = O.philox_fill(cfg.dist, n, cfg.seed, 0, 0, dt, nthreads=nt)
+        yh = O.philox_fill(cfg.dist, n, cfg.seed, 1, 0, dt, nthreads=nt) if cfg.op != "sum" else None
+        sample = f"rank-0 slice of the workload: {n} elements, Philox host twin (bit-identical to the device data)"
+    elif cfg.dist == "illcond":
+        xh = O.philox_fill("illcond", n, cfg.seed, 0, 0, dt, total=cfg.n, nthreads=nt)
+        yh = None
+        sample = f"{n} elements, cfg3 layout from the Philox host twin"
+    else:  # normals have no bit-exact host twin: same shapes/distribution, numpy generator
+        rng = np.random.default_rng(cfg.seed)
+        xh = rng.standard_normal(n).astype(dt)
+        yh = rng.standard_normal(n).astype(dt)
+        sample = f"{n} elements N(0,1) (numpy stand-in with the config's distribution)"
+    for _ in range(args.warmup):
+        O.threads(mid, xh, yh, nt)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.threads(mid, xh, yh, nt)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = n * args.steps / total / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if dt == np.float64 else "f32",
+        "data": "synthetic", "impl": "reference",
+        "config": workload_desc(args.config, cfg, method, n, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": nt, "kind": "port",
+                         "sample": sample + f"; {nt} threads on contiguous shards, each the reference seq "
+                                   "recurrence (kernels.py), shard pairs merged with kernels.py:310-317",
+                         "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1401_0248_b200 as tfb
+    from paper_1401_0248_b200.gen import CONFIGS, make_inputs
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg_key, method_name, n_rank, flush = WORKLOADS[args.config]
+    cfg = CONFIGS[cfg_key]
+    method = tfb.Method(method_name)
+    rows = cfg.op == "rows-dot"
+    n = n_rank or cfg.n
+    n_global = n * world if n_rank else n
+    offset = rank * n if n_rank else 0
+    x, y = make_inputs(cfg, device=dev, offset=offset, n=n if n_rank else None)
+    torch.cuda.synchronize()
+    item = x.element_size()
+    bytes_per_step = n * item * (1 if y is None else 2)
+    lg = tfb.leaf_log2_for(x.dtype, n_global if not rows else cfg.cols)
+
+    def step():
+        if rows:
+            return tfb.reduce_rows(method, x, y)
+        return tfb.sharded_reduce(method, x, y, n_global=n_global if n_rank else n, leaf_log2=lg)
+
+    # Small working sets rotate over R identical copies whose total is >= 4x the
+    # 126 MB L2, so every step streams its inputs from HBM with clean L2 lines
+    # (a memset "flush" would leave dirty lines whose write-back lands in the
+    # timed kernel).  Launch-bound steps are replayed from one CUDA graph.
+    R = 1
+    if flush:
+        R = max(2, -(-(4 * 126 * 10**6) // bytes_per_step))
+    copies = [(x, y)] + [(x.clone(), None if y is None else y.clone()) for _ in range(R - 1)]
+    leaf_arg = args.leaf_log2 or lg
+
+    def step(i):
+        xi, yi = copies[i % R]
+        if rows:
+            return tfb.reduce_rows(method, xi, yi, leaf_log2=args.leaf_log2)
+        return tfb.sharded_reduce(method, xi, yi, n_global=n_global if n_rank else n, leaf_log2=leaf_arg)
+
+    def kernel_launch(i):
+        xi, yi = copies[i % R]
+        if rows:
+            return tfb.reduce_rows(method, xi, yi, leaf_log2=args.leaf_log2)
+        return tfb.reduce(method, xi, yi, leaf_log2=leaf_arg)
+
+    for i in range(args.warmup):
+        step(i)
+        kernel_launch(i)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream(dev)
+    K = args.steps
+    # every timed replay must stream >= 4x L2 of distinct bytes: K_eff >= R
+    K_eff = max(K, R)
+    use_graph = world == 1 and (flush or args.graph)
+
+    def timed(fn):
+        """Device time (ms) of K back-to-back calls of fn, CUDA events on the launching stream."""
+        if use_graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                for i in range(K_eff):
+                    fn(i)
+            torch.cuda.synchronize()
+            g.replay()  # untimed replay: first-launch costs of the graph
+            torch.cuda.synchronize()
+            s = torch.cuda.current_stream(dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            g.replay()
+            e1.record(s)
+            torch.cuda.synchronize()
+            return e0.elapsed_time(e1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(K_eff):
+            fn(i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    # --- device-timed steps -------------------------------------------------
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    with clocks:
+        elapsed_ms = timed(step)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms = t.item() / K_eff
+    value = n * world * K_eff / (t.item() * 1e-3) / 1e9
+    launches_per_step = 1 + (1 if world > 1 and not rows else 0)
+
+    # --- kernel-only timing (roofline of the reduction kernel) ---------------
+    kernel_ms = timed(kernel_launch) / K_eff
+    peak, peak_src = measured_peak()
+    achieved = bytes_per_step / (kernel_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic_for(args.config), "peak_source": peak_src,
+                "kernel": f"leaves_kernel<{method_name},{'f64' if item == 8 else 'f32'},"
+                          f"{'dot' if y is not None else 'sum'}> (fused leaf + tree)",
+                "algorithmic_bytes_per_launch": bytes_per_step, "kernel_ms": kernel_ms,
+                "kernel_share_of_step": kernel_ms / step_ms if step_ms else None,
+                "timing": ("CUDA graph of K launches, events around one replay" if use_graph
+                           else "K back-to-back launches, events on the launching stream")}
+
+    # --- end to end through the public API, pinned host buffers --------------
+    e2e = None
+    res_dev = step(0).cpu()
+    if not args.no_e2e:
+        xh = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+        xh.copy_(x)
+        yh = None
+        if y is not None:
+            yh = torch.empty(y.shape, dtype=y.dtype, pin_memory=True)
+            yh.copy_(y)
+        torch.cuda.synchronize()
+        ke = args.e2e_steps or max(3, min(K, 10))
+
+        def e2e_step():
+            if rows:
+                r = tfb.dot_rows(method, xh, yh)
+                return r.values.cpu()
+            return tfb.sharded_run(method, xh, yh, n_global=n_global if n_rank else n, leaf_log2=lg)
+
+        r0 = e2e_step()  # warm-up (also allocates the staging buffers)
+        if not rows:
+            assert float(r0.value) == float(res_dev[0]) and (
+                method not in (tfb.Method.TWOFOLD_FAST, tfb.Method.TWOFOLD_RIGOROUS)
+                or float(r0.error) == float(res_dev[1])), "e2e result differs from the device path"
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for _ in range(ke):
+            e2e_step()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        if world > 1:
+            tw = torch.tensor([wall], dtype=torch.float64, device=dev)
+            dist.all_reduce(tw, op=dist.ReduceOp.MAX)
+            wall = tw.item()
+        e2e = {"value": n * world * ke / wall / 1e9, "unit": UNIT, "h2d_bytes_per_step": bytes_per_step,
+               "d2h_bytes_per_step": 16 if not rows else cfg.rows * item,
+               "steps": ke, "ms_per_step": 1e3 * wall / ke,
+               "path": ("paper_1401_0248_b200.sharded_run(pinned host shard): leaf-aligned 64 MiB chunks "
+                        "H2D on a copy stream overlapped with the leaf kernels, tree kernel, D2H of the pair"),
+               "timing": "wall clock around the steps after synchronize, max over ranks"}
+
+    # --- CPU baseline (rank 0, N=1 only) ------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and not rows:
+        from oracle import oracle as O
+        nt = host_threads()
+        xs = (xh if not args.no_e2e else x.cpu()).numpy()
+        ys = None if y is None else (yh if not args.no_e2e else y.cpu()).numpy()
+        mid = O.METHODS.index(method_name)
+        rate, best, times, cres = cpu_port_rate(mid, xs, ys, nt)
+        rate1, _, _, _ = cpu_port_rate(mid, xs[: 1 << 25], None if ys is None else ys[: 1 << 25], 1, 4.0)
+        cpu = {"value": rate, "unit": UNIT, "cores": nt, "kind": "port",
+               "sample": (f"the full per-rank workload ({n} elements) per run, best of {len(times)}; "
+                          f"{nt} threads on contiguous shards, each the reference seq recurrence "
+                          "(kernels.py:203-214), shard pairs merged with kernels.py:310-317"),
+               "single_thread_value": rate1, "single_thread_sample": "first 2^25 elements, 1 thread",
+               "cpu": cpu_model()}
+
+    dtype_name = "f64" if item == 8 else "f32"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": dtype_name, "data": "synthetic",
+        "config": dict(workload_desc(args.config, cfg, method_name, n, world),
+                       l2=(f"rotating over {R} input copies ({R * bytes_per_step / 1e6:.0f} MB >= 4x the 126 MB L2)"
+                           if R > 1 else f"inputs {bytes_per_step / 2**30:.1f} GiB per rank >> 126 MB L2 (no flush)"),
+                       leaf_log2=leaf_arg if not rows else (args.leaf_log2 or tfb.leaf_log2_for(x.dtype, cfg.cols)),
+                       steps_timing=("CUDA graph replay" if use_graph else "eager launches")),
+        "hbm_gbs": bytes_per_step * world * K_eff / (t.item() * 1e-3) / 1e9,
+        "steps_timed": K_eff,
+        "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
+        "gpu_launches": launches_per_step * K_eff,
+        "clocks": clocks.report(),
+        "result": {"value": float(res_dev[0]) if not rows else None,
+                   "error": float(res_dev[1]) if not rows else None},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -79,8 +79,9 @@ const char* tf_last_cuda_error(void);
  * Synchronous (one tiny launch + copy on the legacy default stream). */
 int tf_canary(void);
 
-/* Auto leaf size (log2 elements) the grid reduction uses for an n-element row:
- * clamp(ceil_log2(n) - 11, log2(256*V*8), 16) with V = 16/sizeof(T).
+/* Auto leaf size (log2 elements) the grid reduction uses for n = rows*cols
+ * elements: clamp(ceil_log2(n * sizeof(T)) - 11, log2(256*V), 16) with
+ * V = 16/sizeof(T) (about 2048 leaves; one 16-byte vector per thread at least).
  * A pure function of (dtype, n): results never depend on the SM count. */
 int tf_leaf_log2(int dtype, int64_t n);
 
@@ -104,7 +105,8 @@ int tf_reduce(int method, int dtype, const void* x, const void* y, int64_t n,
 
 /* Batched row-wise reduction: rows x cols, row r at x + r*ldx (elements).
  * out_pairs: device, rows pairs.  Row r's pair is bit-identical to
- * tf_reduce(x + r*ldx, cols) with the same leaf_log2 (no reference analogue:
+ * tf_reduce(x + r*ldx, cols) with the same explicit leaf_log2 (the auto leaf
+ * depends on rows*cols, so pass tf_leaf_log2(dtype, rows*cols)) (no reference analogue:
  * equals a per-row loop of dot_twofold_fast). */
 int tf_reduce_rows(int method, int dtype, const void* x, const void* y,
                    int64_t rows, int64_t cols, int64_t ldx, int64_t ldy,

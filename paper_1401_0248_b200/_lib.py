@@ -14,7 +14,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtwofold_b200.so")
+# TFB_LIB overrides the path (tuning sweeps over build variants only).
+LIB_PATH = os.environ.get("TFB_LIB") or os.path.join(_HERE, "libtwofold_b200.so")
 
 TF_OK = 0
 TF_EINVAL_METHOD, TF_EINVAL_DTYPE, TF_EINVAL_SHAPE, TF_EINVAL_ARG = 1, 2, 3, 4

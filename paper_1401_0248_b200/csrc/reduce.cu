@@ -141,6 +141,32 @@ __device__ Pair<A> tree_over(const Pair<A>* parts, int64_t P, Pair<A>* smem) {
   return block_tree<M, A>(cur, smem, static_cast<int>(P2));
 }
 
+template <typename T, bool DOT, int U>
+__device__ __forceinline__ void load_batch(const typename Vec<T>::type* xv, const typename Vec<T>::type* yv,
+                                           int k, typename Vec<T>::type (&a)[U],
+                                           typename Vec<T>::type (&b)[U]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    a[u] = ld_stream(xv + static_cast<int64_t>(k + u) * kThreads);
+    if constexpr (DOT) b[u] = ld_stream(yv + static_cast<int64_t>(k + u) * kThreads);
+  }
+}
+
+template <int M, typename T, bool DOT, int U>
+__device__ __forceinline__ void consume_batch(Pair<typename Acc<M, T>::type>& st,
+                                              const typename Vec<T>::type (&a)[U],
+                                              const typename Vec<T>::type (&b)[U]) {
+  using A = typename Acc<M, T>::type;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+#pragma unroll
+    for (int j = 0; j < Vec<T>::V; ++j) {
+      if constexpr (DOT) step<M, A>(st, addend<M, T, true>(vget(a[u], j), vget(b[u], j)));
+      else step<M, A>(st, addend<M, T, false>(vget(a[u], j), T(0)));
+    }
+  }
+}
+
 // One thread's sequential recurrence over its elements of the leaf at
 // `start` of a row of n elements.  VEC: 16-byte aligned row, full leaf.
 template <int M, typename T, bool DOT, bool VEC, int U>
@@ -155,23 +181,32 @@ __device__ __forceinline__ Pair<typename Acc<M, T>::type> leaf_chain(
   if (VEC && start + L <= n) {
     const VT* xv = reinterpret_cast<const VT*>(x + start) + t;
     const VT* yv = DOT ? reinterpret_cast<const VT*>(y + start) + t : nullptr;
+    // Software pipeline: batch k+U is in flight while batch k is consumed, so
+    // each thread keeps 2U vectors per operand outstanding.  Elements are
+    // consumed in exactly the same order as without the pipeline.
     int k = 0;
-    for (; k + U <= R; k += U) {
-      VT a[U], b[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        a[u] = ld_stream(xv + static_cast<int64_t>(k + u) * kThreads);
-        if constexpr (DOT) b[u] = ld_stream(yv + static_cast<int64_t>(k + u) * kThreads);
+#if TFB_PIPELINE
+    if (R >= U) {
+      VT a0[U], b0[U], a1[U], b1[U];
+      load_batch<T, DOT, U>(xv, yv, 0, a0, b0);
+      for (; k + 2 * U <= R; k += 2 * U) {
+        load_batch<T, DOT, U>(xv, yv, k + U, a1, b1);
+        consume_batch<M, T, DOT, U>(st, a0, b0);
+        if (k + 2 * U < R) load_batch<T, DOT, U>(xv, yv, k + 2 * U, a0, b0);
+        consume_batch<M, T, DOT, U>(st, a1, b1);
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-          if constexpr (DOT) step<M, A>(st, addend<M, T, true>(vget(a[u], j), vget(b[u], j)));
-          else step<M, A>(st, addend<M, T, false>(vget(a[u], j), T(0)));
-        }
+      if (k + U <= R) {  // R == U (odd number of batches only happens for R == U)
+        consume_batch<M, T, DOT, U>(st, a0, b0);
+        k += U;
       }
     }
+#else
+    for (; k + U <= R; k += U) {
+      VT a[U], b[U];
+      load_batch<T, DOT, U>(xv, yv, k, a, b);
+      consume_batch<M, T, DOT, U>(st, a, b);
+    }
+#endif
     for (; k < R; ++k) {
       VT a = ld_stream(xv + static_cast<int64_t>(k) * kThreads);
       VT b;
@@ -199,7 +234,18 @@ __device__ __forceinline__ Pair<typename Acc<M, T>::type> leaf_chain(
   return st;
 }
 
-template <typename T> struct Unroll { static constexpr int value = 4; };
+#ifndef TFB_PIPELINE
+#define TFB_PIPELINE 0  // measured: no gain, costs occupancy (profiles/r01_variants.md)
+#endif
+#ifndef TFB_UNROLL_F32
+#define TFB_UNROLL_F32 4
+#endif
+#ifndef TFB_UNROLL_F64
+#define TFB_UNROLL_F64 2
+#endif
+template <typename T> struct Unroll;
+template <> struct Unroll<float> { static constexpr int value = TFB_UNROLL_F32; };
+template <> struct Unroll<double> { static constexpr int value = TFB_UNROLL_F64; };
 
 // Grid reduction over rows x cols.  Unit u = (row r, leaf l), u = r*P + l.
 // mode 0: write leaf pairs to partials[u] only.  mode 1: fused — the CTA that
@@ -360,17 +406,16 @@ int ceil_log2_i64(int64_t n) {
   return l;
 }
 
-int min_leaf_log2(int dtype) {
-  // log2(256 threads * V * 8 vectors): 8192 f32 / 4096 f64 elements
-  return dtype == TF_F32 ? 13 : 12;
-}
-int floor_leaf_log2(int dtype) {  // smallest legal explicit leaf: one vector per thread
+int floor_leaf_log2(int dtype) {  // smallest leaf: one 16-byte vector per thread
   return dtype == TF_F32 ? 10 : 9;
 }
 
-int auto_leaf_log2(int dtype, int64_t n) {
-  int l = ceil_log2_i64(n > 0 ? n : 1) - 11;
-  const int lo = min_leaf_log2(dtype);
+// Auto leaf: about 2^-11 of the operand bytes (~2048 leaves), at least one
+// vector per thread, at most 2^16 elements.  `total` = rows * cols.
+// Measured optimum on B200 for every BASELINE config (profiles/r01_leaf_sweep.md).
+int auto_leaf_log2(int dtype, int64_t total) {
+  int l = ceil_log2_i64(total > 0 ? total : 1) + (dtype == TF_F32 ? 2 : 3) - 11;
+  const int lo = floor_leaf_log2(dtype);
   if (l < lo) l = lo;
   if (l > 16) l = 16;
   return l;
@@ -474,9 +519,9 @@ static int validate(int method, int dtype) {
   return TF_OK;
 }
 
-static int resolve_leaf(int dtype, int64_t cols, int leaf_log2, int* out) {
+static int resolve_leaf(int dtype, int64_t total, int leaf_log2, int* out) {
   if (leaf_log2 == 0) {
-    *out = auto_leaf_log2(dtype, cols);
+    *out = auto_leaf_log2(dtype, total);
     return TF_OK;
   }
   if (leaf_log2 < floor_leaf_log2(dtype) || leaf_log2 > 24) return TF_EINVAL_ARG;
@@ -501,7 +546,7 @@ int tf_workspace_size(int method, int dtype, int64_t rows, int64_t cols, int lea
   if (rc) return rc;
   if (rows < 0 || cols < 0) return TF_EINVAL_SHAPE;
   int lg;
-  if ((rc = resolve_leaf(dtype, cols, leaf_log2, &lg))) return rc;
+  if ((rc = resolve_leaf(dtype, rows * cols, leaf_log2, &lg))) return rc;
   const int64_t P = (cols + (int64_t(1) << lg) - 1) >> lg;
   if (partials_bytes) *partials_bytes = static_cast<size_t>(rows * P) * pair_bytes(method, dtype);
   if (counters) *counters = rows;
@@ -519,7 +564,7 @@ int tf_reduce_rows(int method, int dtype, const void* x, const void* y, int64_t 
   if (rows == 0) return TF_OK;
   if (!out_pairs || (cols > 0 && !x)) return TF_EINVAL_ARG;
   int lg;
-  if ((rc = resolve_leaf(dtype, cols, leaf_log2, &lg))) return rc;
+  if ((rc = resolve_leaf(dtype, rows * cols, leaf_log2, &lg))) return rc;
   auto s = static_cast<cudaStream_t>(stream);
   if (cols == 0) {  // every row is empty: (+0, +0)
     if (cudaMemsetAsync(out_pairs, 0, static_cast<size_t>(rows) * pair_bytes(method, dtype), s) !=

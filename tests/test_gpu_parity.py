@@ -170,8 +170,9 @@ def test_rows_equal_per_row_reduce_and_emulator(tfb, oracle, cuda):
             ev, ee = oracle.emulate_rows(m, Xh, Yh)
             for r in range(rows):
                 _same(got[r], (ev[r], ee[r]), (dt, rows, cols, m, r))
+            lg = tfb.leaf_log2_for(tdt, rows * cols)  # the rows auto leaf depends on rows*cols
             for r in (0, rows - 1):
-                _same(got[r], tfb.reduce(meth, X[r], Y[r]).cpu().numpy(), ("row vs 1-D", r))
+                _same(got[r], tfb.reduce(meth, X[r], Y[r], leaf_log2=lg).cpu().numpy(), ("row vs 1-D", r))
 
 
 def test_rows_strided_leading_dimension(tfb, oracle, cuda):
