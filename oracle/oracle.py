@@ -230,15 +230,24 @@ def deviation(v, e, S: Fraction) -> Fraction:
     return abs(Fraction(float(v)) + Fraction(float(e)) - S)
 
 
+def calibrated_fast_bound(dtype, n: int, A: Fraction) -> Fraction:
+    """2 N eps^2 A + 2^-6 eps A: SURVEY.md §8(c)'s calibrated twofold-fast tolerance
+    for random BASELINE-size data (not a theorem; checked at N >= 2^16)."""
+    eps = Fraction(EPS[np.dtype(dtype)])
+    return 2 * n * eps * eps * A + Fraction(1, 64) * eps * A
+
+
 def bound(method: int, dtype, n: int, A: Fraction, chain: int | None = None) -> Fraction:
     """Accuracy bound for the GPU flavor of `method` on n addends with A = sum|y|."""
     eps = Fraction(EPS[np.dtype(dtype)])
     if method == M_RIGOROUS:
         return 2 * n * eps * eps * A
     if method == M_FAST:
-        # no rigorous bound: Dekker's precondition can fail on signed data
-        # (PAPER.md:247); calibrated extra term 2^-6 eps A (SURVEY.md §8(c))
-        return 2 * n * eps * eps * A + Fraction(1, 64) * eps * A
+        # Dekker's precondition |s| >= |y| can fail on signed data (PAPER.md:247);
+        # each failure can lose at most about its own round-off (<= eps |y_i|),
+        # hence the loose first-order term.  calibrated_fast_bound() is the tight
+        # empirical one (SURVEY.md §8(c)) used at BASELINE sizes.
+        return 2 * n * eps * eps * A + eps * A
     if method == M_KAHAN:
         return (2 * eps + 2 * n * eps * eps) * A
     # direct / wide: gamma_h with h = per-thread chain + tree depth

@@ -1,0 +1,71 @@
+"""The C-ABI library loads without a GPU and exports every symbol include/*.h declares."""
+
+import ctypes
+import os
+import re
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(REPO, "include", "twofold_b200.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\*?\s+\*?(tf_\w+)\s*\(", src, flags=re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_1401_0248_b200 import _lib
+    return _lib.lib()
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("tf_reduce", "tf_reduce_rows", "tf_reduce_leaves", "tf_merge_tree", "tf_reduce_seq",
+                 "tf_reduce_lanes", "tf_eft", "tf_fill", "tf_fill_rows_scaled", "tf_canary", "tf_strerror",
+                 "tf_workspace_size", "tf_leaf_log2", "tf_version", "tf_last_cuda_error"):
+        assert must in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    raw = ctypes.CDLL(lib._name)
+    for name in declared_functions():
+        assert hasattr(raw, name), name
+
+
+def test_host_only_entry_points(lib, oracle):
+    from paper_1401_0248_b200 import _lib
+    assert lib.tf_version() >= 1
+    assert lib.tf_strerror(_lib.TF_EINVAL_DTYPE).decode().startswith("unsupported dtype")
+    for dt in (0, 1):
+        for n in (0, 1, 2, 1000, 1 << 16, (1 << 20) + 1, 1 << 24, 1 << 29, 1 << 32, 1 << 40):
+            assert lib.tf_leaf_log2(dt, n) == oracle.lib().tfo_leaf_log2(dt, n), (dt, n)
+
+
+def test_validation_before_any_device_work(lib):
+    from paper_1401_0248_b200 import _lib
+    # argument errors are reported without touching the GPU (none here)
+    assert lib.tf_reduce(9, 0, None, None, 10, 0, None, None, 0, None, 0, None) == _lib.TF_EINVAL_METHOD
+    assert lib.tf_reduce(1, 1, None, None, 10, 0, None, None, 0, None, 0, None) == _lib.TF_EINVAL_DTYPE
+    assert lib.tf_reduce(2, 5, None, None, 10, 0, None, None, 0, None, 0, None) == _lib.TF_EINVAL_DTYPE
+    assert lib.tf_reduce(2, 1, None, None, -1, 0, None, None, 0, None, 0, None) == _lib.TF_EINVAL_SHAPE
+    assert lib.tf_reduce_lanes(2, 1, None, None, 8, 3, None, None) == _lib.TF_EINVAL_ARG
+    assert lib.tf_reduce_lanes(2, 1, None, None, 8, 32, None, None) == _lib.TF_EINVAL_ARG
+    assert lib.tf_reduce(2, 1, None, None, 10, 3, None, None, 0, None, 0, None) == _lib.TF_EINVAL_ARG
+    assert lib.tf_fill(7, 1, 0, 0, 0, 10, 0, 0, 0, 0, None, None) == _lib.TF_EINVAL_ARG
+    # multi-leaf input without scratch
+    assert lib.tf_reduce(2, 1, 16, None, 1 << 20, 0, 16, None, 0, None, 0, None) == _lib.TF_EWORKSPACE
+
+
+def test_workspace_size(lib):
+    from paper_1401_0248_b200 import Method, workspace_size
+    import torch
+    pb, cnt, leaves = workspace_size(Method.TWOFOLD_FAST, torch.float64, 1, 1 << 29)
+    assert leaves == (1 << 29) >> 16 and pb == leaves * 16 and cnt == 1
+    pb, cnt, leaves = workspace_size(Method.WIDE, torch.float32, 4096, 65536)
+    assert leaves == 1 and pb == 4096 * 16 and cnt == 4096  # wide pairs are binary64
+    pb, cnt, leaves = workspace_size(Method.KAHAN, torch.float32, 1, 1 << 24)
+    assert leaves == (1 << 24) >> 15 and pb == leaves * 8

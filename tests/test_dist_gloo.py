@@ -1,0 +1,113 @@
+"""Multi-rank shard/combine plumbing on CPU: world_size 2 (and 4) over gloo.
+
+The product's local reducer and merge are CUDA kernels; here they are
+injected with the oracle's bit-exact restatements of those kernels, so the
+test exercises exactly dist.py's sharding, all-gather order and merge
+placement.  With a power-of-two layout the sharded result must equal the
+single-device result bit for bit, on every rank.
+"""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, dtype_name, q):
+    sys.path.insert(0, REPO)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    import paper_1401_0248_b200 as tfb
+
+    dt = np.float32 if dtype_name == "f32" else np.float64
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    x = O.lcg_fill("mmix", n, 17, dt, True)
+    y = O.lcg_fill("nr", n, 18, dt, True)
+    lg = tfb.leaf_log2_for(tdt, n)
+    a, b = tfb.shard_range(n, rank, world, lg)
+    xs, ys = torch.from_numpy(x[a:b].copy()), torch.from_numpy(y[a:b].copy())
+
+    def local(method, xl, yl, leaf):
+        mid = list(tfb.Method).index(method)
+        v, e = O.emulate(mid, xl.numpy(), None if yl is None else yl.numpy(), leaf)
+        return torch.tensor([float(v), float(e)], dtype=torch.float64 if method is tfb.Method.WIDE else tdt)
+
+    def merge(method, pairs):
+        mid = list(tfb.Method).index(method)
+        v, e = O.tree(mid, np.float64 if method is tfb.Method.WIDE else dt, pairs[:, 0].numpy(), pairs[:, 1].numpy())
+        return torch.tensor([float(v), float(e)], dtype=pairs.dtype)
+
+    out = {}
+    for method in tfb.Method:
+        if method is tfb.Method.WIDE and dt != np.float32:
+            continue
+        pair = tfb.sharded_reduce(method, xs, ys, n_global=n, local_reduce=local, merge=merge)
+        res = tfb.sharded_run(method, xs, None, n_global=n, local_reduce=local, merge=merge)
+        out[method.value] = (pair.tolist(), float(res.value), float(res.error), type(res.value).__name__,
+                             res.adds_performed)
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _run(world, n, dtype_name):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, dtype_name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return results
+
+
+@pytest.mark.parametrize("world,dtype_name", [(2, "f64"), (2, "f32"), (4, "f64")])
+def test_sharded_equals_single_device_tree(oracle, world, dtype_name):
+    n = 1 << 18
+    results = _run(world, n, dtype_name)
+    dt = np.float32 if dtype_name == "f32" else np.float64
+    x = oracle.lcg_fill("mmix", n, 17, dt, True)
+    y = oracle.lcg_fill("nr", n, 18, dt, True)
+    for method_name, (pair, v, e, tname, adds) in results[0].items():
+        mid = oracle.METHODS.index(method_name)
+        want = oracle.emulate(mid, x, y)
+        assert [float(want[0]), float(want[1])] == pair, method_name
+        # all ranks hold the identical result
+        for r in range(1, world):
+            assert results[r][method_name] == results[0][method_name]
+        # SumResult conventions: typed like the data (f64 for wide), error 0 for non-twofold
+        ws = oracle.emulate(mid, x)
+        assert v == float(ws[0])
+        assert e == (float(ws[1]) if mid in (2, 3) else 0.0)
+        assert tname == ("float64" if mid == 1 else np.dtype(dt).name)
+        assert adds == n
+
+
+def test_ragged_shards_cover_everything(oracle):
+    """Non-power-of-two n: shards are leaf-aligned and the merged pair still tracks the exact sum."""
+    n = 300_007
+    results = _run(2, n, "f64")
+    x = oracle.lcg_fill("mmix", n, 17, np.float64, True)
+    y = oracle.lcg_fill("nr", n, 18, np.float64, True)
+    S, A = oracle.exact(x, y), oracle.abs_sum(x, y)
+    pair = results[0]["twofold-rigorous"][0]
+    assert oracle.deviation(pair[0], pair[1], S) <= oracle.bound(3, np.float64, n, A)

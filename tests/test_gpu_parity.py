@@ -155,6 +155,8 @@ def test_tolerances_against_exact_oracle(tfb, oracle, cuda):
                 dev = oracle.deviation(pair[0], 0.0, S)
             chain = (1 << tfb.leaf_log2_for(tdt, n)) // 256 + 30
             assert dev <= oracle.bound(m, dt, n, A, chain=chain), (dist, dt, m, float(dev))
+            if m == 2:  # twofold-fast: the calibrated tolerance of SURVEY.md §8(c) at these sizes
+                assert dev <= oracle.calibrated_fast_bound(dt, n, A), (dist, dt, float(dev))
 
 
 def test_rows_equal_per_row_reduce_and_emulator(tfb, oracle, cuda):

@@ -1,0 +1,72 @@
+"""Codegen guard (the device analogue of the fast-math canary, kernels.py:545-568).
+
+Every reduction kernel must be built from separate IEEE adds/multiplies: a
+contracted FFMA/DFMA in a reduction path would change the dot products'
+rounding (the reference rounds each product, kernels.py:23-26) and an
+FTZ/fast-math build would zero the error channel.  The hot kernels must use
+the 128-bit streaming load path.
+"""
+
+import os
+import re
+import shutil
+import subprocess
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SO = os.path.join(REPO, "paper_1401_0248_b200", "libtwofold_b200.so")
+
+
+@pytest.fixture(scope="module")
+def sass():
+    if not shutil.which("cuobjdump"):
+        pytest.skip("cuobjdump not installed")
+    out = subprocess.run(["cuobjdump", "-sass", SO], check=True, capture_output=True, text=True).stdout
+    funcs = {}
+    cur = None
+    for line in out.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            cur = m.group(1)
+            funcs[cur] = []
+        elif cur:
+            funcs[cur].append(line)
+    return funcs
+
+
+REDUCTION = ("leaves_kernel", "tree_kernel", "seq_kernel", "lanes_kernel", "canary_kernel", "eft_kernel")
+
+
+def test_sm100a_code_present(sass):
+    assert any("leaves_kernel" in f for f in sass)
+    arch = subprocess.run(["cuobjdump", "-lelf", SO], capture_output=True, text=True).stdout
+    assert "sm_100a" in arch
+
+
+def test_no_fused_multiply_add_in_reduction_kernels(sass):
+    bad = []
+    for fn, lines in sass.items():
+        if any(k in fn for k in REDUCTION):
+            for ln in lines:
+                if re.search(r"\b(FFMA|DFMA|FFMA2)\b", ln):
+                    bad.append((fn, ln.strip()))
+                # HFMA2 Rd, -RZ, RZ, imm is ptxas's register-move idiom, not arithmetic
+                elif re.search(r"\bHFMA2\b", ln) and "-RZ, RZ" not in ln:
+                    bad.append((fn, ln.strip()))
+    assert not bad, bad[:5]
+
+
+def test_no_flush_to_zero_arithmetic(sass):
+    for fn, lines in sass.items():
+        if any(k in fn for k in REDUCTION):
+            # floating-point arithmetic must keep subnormals (F2I.FTZ of the integer
+            # division idiom is a conversion, not data arithmetic)
+            assert not any(re.search(r"\b(FADD|FMUL|DADD|DMUL|FSETP|FMNMX)\S*\.FTZ", ln) for ln in lines), fn
+
+
+def test_streaming_128bit_loads_in_vector_kernels(sass):
+    vec = [fn for fn in sass if "leaves_kernel" in fn and fn.endswith("ELb1EEEvPKT0_S3_llllilPNS_4PairINS_3AccIXT_ES1_E4typeEEEPjS9_i")]
+    assert vec
+    for fn in vec:
+        assert any(re.search(r"LDG\.E\.(NA\.)?\S*128", ln) for ln in sass[fn]), fn
