@@ -56,6 +56,14 @@ extern "C" {
 #define TF_TWOFOLD_RIGOROUS  3  /* sumt / dott          kernels.py:157-170, :217-230 */
 #define TF_KAHAN             4  /* sumk / dotk          kernels.py:173-183, :233-243 */
 
+/* Opt-in flag OR-ed into TF_TWOFOLD_FAST / TF_TWOFOLD_RIGOROUS for dot products:
+ * TwoProduct — the product's exact round-off fma(a, b, -fl(a*b)) is added to the
+ * error channel, so value + error tracks the exact dot of the TRUE products
+ * (Ogita-Rump-Oishi Dot2 style).  Not in the reference, which rounds every
+ * product and tracks only summation round-off (kernels.py:23-26).
+ * Invalid (TF_EINVAL_ARG) for sums and other methods. */
+#define TF_TRACK_PRODUCT 0x100
+
 /* Data types. */
 #define TF_F32 0
 #define TF_F64 1

@@ -24,6 +24,7 @@ _LIB_PATH = os.path.join(_HERE, "build", "libtfo.so")
 
 METHODS = ("direct", "wide", "twofold-fast", "twofold-rigorous", "kahan")
 M_DIRECT, M_WIDE, M_FAST, M_RIGOROUS, M_KAHAN = range(5)
+M_FAST_TP, M_RIGOROUS_TP = 5, 6  # opt-in TwoProduct dots (tf_* method | TF_TRACK_PRODUCT)
 EPS = {np.dtype(np.float32): 2.0 ** -24, np.dtype(np.float64): 2.0 ** -53}
 
 _lib = None
@@ -78,7 +79,7 @@ def _prep(x, y):
     return x, y, (None if y is None else y.ctypes.data)
 
 
-def _acc_type(method: int, dtype):
+def _acc_type(method: int, dtype):  # noqa: D103
     return np.float64 if method == M_WIDE else np.dtype(dtype).type
 
 
@@ -166,11 +167,13 @@ def leaf_log2_auto(dtype, n: int) -> int:
     return lib().tfo_leaf_log2(0 if np.dtype(dtype) == np.float32 else 1, n)
 
 
-def exact_components(x, y=None, absolute: bool = False, cap: int = 128) -> tuple:
-    """Exact expansion (expansion.py:79-101) of the identical addends y_i."""
+def exact_components(x, y=None, absolute: bool = False, cap: int = 128, true_products: bool = False) -> tuple:
+    """Exact expansion (expansion.py:79-101) of the identical addends y_i
+    (true_products: of the exact products a_i*b_i, the TwoProduct target)."""
     x, y, yp = _prep(x, y)
     comp = np.zeros(cap, np.float64)
-    m = lib().tfo_exact(_dt(x), x.ctypes.data, yp, x.shape[0], 1 if absolute else 0,
+    mode = (1 if absolute else 0) | (2 if true_products else 0)
+    m = lib().tfo_exact(_dt(x), x.ctypes.data, yp, x.shape[0], mode,
                         comp.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cap)
     assert m >= 0, "expansion overflow"
     return tuple(float(c) for c in comp[:m])
@@ -190,6 +193,15 @@ def exact(x, y=None) -> Fraction:
 
 def abs_sum(x, y=None) -> Fraction:
     return sum((Fraction(c) for c in exact_components(x, y, absolute=True)), Fraction(0))
+
+
+def exact_true_dot(x, y) -> Fraction:
+    """Exact sum of the exact products (what a TwoProduct dot tracks)."""
+    return sum((Fraction(c) for c in exact_components(x, y, true_products=True)), Fraction(0))
+
+
+def abs_true_dot(x, y) -> Fraction:
+    return sum((Fraction(c) for c in exact_components(x, y, absolute=True, true_products=True)), Fraction(0))
 
 
 def lcg_fill(kind: str, n: int, seed: int = 1, dtype=np.float64, sym: bool = False) -> np.ndarray:

@@ -45,6 +45,20 @@ class Method(Enum):
 
 _METHOD_ID = {Method.DIRECT: 0, Method.WIDE: 1, Method.TWOFOLD_FAST: 2,
               Method.TWOFOLD_RIGOROUS: 3, Method.KAHAN: 4}
+TRACK_PRODUCT = 0x100  # TF_TRACK_PRODUCT: opt-in TwoProduct dots (include/twofold_b200.h)
+
+
+def _mid(method: Method, track_product: bool = False, dot: bool = True) -> int:
+    """C-ABI method id; track_product adds the exact product round-off to the
+    error channel (Dot2-style; the reference tracks summation round-off only,
+    kernels.py:23-26), valid for twofold dot products."""
+    if not track_product:
+        return _METHOD_ID[method]
+    if method not in (Method.TWOFOLD_FAST, Method.TWOFOLD_RIGOROUS):
+        raise ValueError("track_product needs a twofold method")
+    if not dot:
+        raise ValueError("track_product applies to dot products")
+    return _METHOD_ID[method] | TRACK_PRODUCT
 _TWOFOLD_METHODS = (Method.TWOFOLD_FAST, Method.TWOFOLD_RIGOROUS)
 
 _LANE_RANGE = (2, 16)
@@ -275,7 +289,7 @@ def leaf_log2_for(dtype: torch.dtype, n: int) -> int:
 # Device-side launchers (asynchronous; return device pairs).
 
 def _reduce_grid(method: Method, x: torch.Tensor, y: torch.Tensor | None, leaf_log2: int = 0,
-                 out: torch.Tensor | None = None) -> torch.Tensor:
+                 out: torch.Tensor | None = None, track_product: bool = False) -> torch.Tensor:
     dev = x.device
     _lib.ensure_canary(dev.index)
     acc = _acc_dtype(method, x.dtype)
@@ -286,15 +300,17 @@ def _reduce_grid(method: Method, x: torch.Tensor, y: torch.Tensor | None, leaf_l
     parts = ctrs = None
     if leaves > 1:
         parts, ctrs = _scratch.get(dev, pb, cnt)
-    check(lib().tf_reduce(_METHOD_ID[method], _dtype_code(x.dtype), _ptr(x), _ptr(y), n, leaf_log2,
+    check(lib().tf_reduce(_mid(method, track_product, y is not None), _dtype_code(x.dtype), _ptr(x), _ptr(y), n,
+                          leaf_log2,
                           out.data_ptr(), _ptr(parts), pb, _ptr(ctrs), cnt, _stream_ptr(dev)),
           "tf_reduce")
     return out
 
 
 def _reduce_leaves(method: Method, x: torch.Tensor, y: torch.Tensor | None, leaf_log2: int,
-                   partials_ptr: int, stream_ptr: int) -> None:
-    check(lib().tf_reduce_leaves(_METHOD_ID[method], _dtype_code(x.dtype), _ptr(x), _ptr(y), x.numel(),
+                   partials_ptr: int, stream_ptr: int, track_product: bool = False) -> None:
+    check(lib().tf_reduce_leaves(_mid(method, track_product, y is not None), _dtype_code(x.dtype), _ptr(x),
+                                 _ptr(y), x.numel(),
                                  leaf_log2, partials_ptr, stream_ptr), "tf_reduce_leaves")
 
 
@@ -333,7 +349,7 @@ _copy_streams = _CopyStreams()
 
 
 def _reduce_grid_host(method: Method, x: torch.Tensor, y: torch.Tensor | None, dev: torch.device,
-                      leaf_log2: int = 0) -> torch.Tensor:
+                      leaf_log2: int = 0, track_product: bool = False) -> torch.Tensor:
     """Grid flavor for host inputs: leaf-aligned chunks are copied H2D on a side
     stream (double-buffered) while the previous chunk's leaves reduce; the
     final tree runs over all leaf pairs — bit-identical to the device path."""
@@ -344,7 +360,7 @@ def _reduce_grid_host(method: Method, x: torch.Tensor, y: torch.Tensor | None, d
     item = x.element_size()
     chunk_leaves = max(1, _CHUNK_BYTES // (L * item))
     if P <= chunk_leaves:
-        return _reduce_grid(method, _on_device(x, dev), _on_device(y, dev), lg)
+        return _reduce_grid(method, _on_device(x, dev), _on_device(y, dev), lg, track_product=track_product)
     _lib.ensure_canary(dev.index)
     acc = _acc_dtype(method, x.dtype)
     pair_bytes = 2 * torch.empty(0, dtype=acc).element_size()
@@ -369,7 +385,7 @@ def _reduce_grid_host(method: Method, x: torch.Tensor, y: torch.Tensor | None, d
             ready[b].record(copy)
         compute.wait_event(ready[b])
         _reduce_leaves(method, xs[b][: hi - lo], None if y is None else ys[b][: hi - lo], lg,
-                       partials.data_ptr() + c * chunk_leaves * pair_bytes, compute.cuda_stream)
+                       partials.data_ptr() + c * chunk_leaves * pair_bytes, compute.cuda_stream, track_product)
         free[b].record(compute)
     for t in xs + (ys or []):
         t.record_stream(copy)
@@ -379,41 +395,42 @@ def _reduce_grid_host(method: Method, x: torch.Tensor, y: torch.Tensor | None, d
     return out
 
 
-def _reduce_seq(method: Method, x, y, dev) -> torch.Tensor:
+def _reduce_seq(method: Method, x, y, dev, track_product: bool = False) -> torch.Tensor:
     _lib.ensure_canary(dev.index)
     out = torch.empty(2, dtype=_acc_dtype(method, x.dtype), device=dev)
-    check(lib().tf_reduce_seq(_METHOD_ID[method], _dtype_code(x.dtype), _ptr(x), _ptr(y), x.numel(),
+    check(lib().tf_reduce_seq(_mid(method, track_product, y is not None), _dtype_code(x.dtype), _ptr(x), _ptr(y), x.numel(),
                               out.data_ptr(), _stream_ptr(dev)), "tf_reduce_seq")
     return out
 
 
-def _reduce_lanes(method: Method, x, y, k: int, dev) -> torch.Tensor:
+def _reduce_lanes(method: Method, x, y, k: int, dev, track_product: bool = False) -> torch.Tensor:
     _lib.ensure_canary(dev.index)
     out = torch.empty(2, dtype=_acc_dtype(method, x.dtype), device=dev)
-    check(lib().tf_reduce_lanes(_METHOD_ID[method], _dtype_code(x.dtype), _ptr(x), _ptr(y), x.numel(), k,
+    check(lib().tf_reduce_lanes(_mid(method, track_product, y is not None), _dtype_code(x.dtype), _ptr(x), _ptr(y), x.numel(), k,
                                 out.data_ptr(), _stream_ptr(dev)), "tf_reduce_lanes")
     return out
 
 
 def reduce(method: Method, data, b=None, *, flavor: Flavor = _CUDA, leaf_log2: int = 0,
-           out: torch.Tensor | None = None) -> torch.Tensor:
+           out: torch.Tensor | None = None, track_product: bool = False) -> torch.Tensor:
     """Asynchronous form of run_flavor: returns the raw (value, error) pair as a
     2-element device tensor without synchronizing (for KAHAN the error slot
     holds the pending compensation).  Inputs must already be CUDA tensors for
-    the result to stay asynchronous."""
+    the result to stay asynchronous.  track_product: opt-in TwoProduct dot."""
     x, y = _check_input(data, b)
     if method is Method.WIDE and x.dtype != torch.float32:
         raise TypeError("wide accumulation is defined for float32 data only")
+    _mid(method, track_product, y is not None)  # validate before touching the device
     dev = _device_for(x)
     if flavor.kind == "cuda":
         if x.is_cuda:
-            return _reduce_grid(method, _on_device(x, dev), _on_device(y, dev), leaf_log2, out)
-        return _reduce_grid_host(method, x, y, dev, leaf_log2)
+            return _reduce_grid(method, _on_device(x, dev), _on_device(y, dev), leaf_log2, out, track_product)
+        return _reduce_grid_host(method, x, y, dev, leaf_log2, track_product)
     xd, yd = _on_device(x, dev), _on_device(y, dev)
     if flavor.kind == "seq":
-        return _reduce_seq(method, xd, yd, dev)
+        return _reduce_seq(method, xd, yd, dev, track_product)
     k = flavor.lanes or _DEFAULT_LANES[np.dtype(_np_type(x.dtype))]
-    return _reduce_lanes(method, xd, yd, k, dev)
+    return _reduce_lanes(method, xd, yd, k, dev, track_product)
 
 
 def _finish(method: Method, pair: torch.Tensor, dtype: torch.dtype, n: int) -> SumResult:
@@ -424,7 +441,7 @@ def _finish(method: Method, pair: torch.Tensor, dtype: torch.dtype, n: int) -> S
     return SumResult(Twofold(t(v), t(0)), n)
 
 
-def run_flavor(method: Method, flavor: Flavor, data, b=None) -> SumResult:
+def run_flavor(method: Method, flavor: Flavor, data, b=None, *, track_product: bool = False) -> SumResult:
     """Run one method in one flavor over data (dot product when b is given).
 
     Mirrors kernels.py:591-640: same validation order and exceptions, result
@@ -439,7 +456,7 @@ def run_flavor(method: Method, flavor: Flavor, data, b=None) -> SumResult:
         raise TypeError("wide accumulation is defined for float32 data only")
     if method not in _METHOD_ID:
         raise ValueError(f"unknown method {method!r}")
-    pair = reduce(method, x, y, flavor=flavor)
+    pair = reduce(method, x, y, flavor=flavor, track_product=track_product)
     return _finish(method, pair, x.dtype, n)
 
 
@@ -487,12 +504,12 @@ def dot_wide(a, b) -> SumResult:
     return run_flavor(Method.WIDE, _CUDA, a, b)
 
 
-def dot_twofold_fast(a, b) -> SumResult:
-    return run_flavor(Method.TWOFOLD_FAST, _CUDA, a, b)
+def dot_twofold_fast(a, b, *, track_product: bool = False) -> SumResult:
+    return run_flavor(Method.TWOFOLD_FAST, _CUDA, a, b, track_product=track_product)
 
 
-def dot_twofold_rigorous(a, b) -> SumResult:
-    return run_flavor(Method.TWOFOLD_RIGOROUS, _CUDA, a, b)
+def dot_twofold_rigorous(a, b, *, track_product: bool = False) -> SumResult:
+    return run_flavor(Method.TWOFOLD_RIGOROUS, _CUDA, a, b, track_product=track_product)
 
 
 def dot_kahan(a, b) -> SumResult:
@@ -514,7 +531,7 @@ def _as_rows(a) -> torch.Tensor:
 
 
 def reduce_rows(method: Method, X, Y=None, *, leaf_log2: int = 0,
-                out: torch.Tensor | None = None) -> torch.Tensor:
+                out: torch.Tensor | None = None, track_product: bool = False) -> torch.Tensor:
     """Asynchronous row-wise reduction: returns a (rows, 2) device tensor of raw pairs.
     Row r is bit-identical to reduce(method, X[r], Y[r]) with the same leaf size."""
     x = _as_rows(X)
@@ -526,6 +543,7 @@ def reduce_rows(method: Method, X, Y=None, *, leaf_log2: int = 0,
             raise ValueError("dot operands must have equal shapes")
     if method is Method.WIDE and x.dtype != torch.float32:
         raise TypeError("wide accumulation is defined for float32 data only")
+    mid = _mid(method, track_product, y is not None)
     dev = _device_for(x)
     if not x.is_cuda:
         x = x.to(dev, non_blocking=x.is_pinned())
@@ -540,7 +558,7 @@ def reduce_rows(method: Method, X, Y=None, *, leaf_log2: int = 0,
     parts = ctrs = None
     if leaves > 1:
         parts, ctrs = _scratch.get(dev, pb, cnt)
-    check(lib().tf_reduce_rows(_METHOD_ID[method], _dtype_code(x.dtype), _ptr(x), _ptr(y), rows, cols,
+    check(lib().tf_reduce_rows(mid, _dtype_code(x.dtype), _ptr(x), _ptr(y), rows, cols,
                                x.stride(0), 0 if y is None else y.stride(0), leaf_log2, out.data_ptr(),
                                _ptr(parts), pb, _ptr(ctrs), cnt, _stream_ptr(dev)), "tf_reduce_rows")
     return out
@@ -556,8 +574,8 @@ def sum_rows(method: Method, X, *, leaf_log2: int = 0) -> RowsResult:
     return _rows_result(method, pairs, _as_rows(X).shape[1])
 
 
-def dot_rows(method: Method, X, Y, *, leaf_log2: int = 0) -> RowsResult:
-    pairs = reduce_rows(method, X, Y, leaf_log2=leaf_log2)
+def dot_rows(method: Method, X, Y, *, leaf_log2: int = 0, track_product: bool = False) -> RowsResult:
+    pairs = reduce_rows(method, X, Y, leaf_log2=leaf_log2, track_product=track_product)
     return _rows_result(method, pairs, _as_rows(X).shape[1])
 
 

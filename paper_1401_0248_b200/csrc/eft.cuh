@@ -19,18 +19,32 @@
 
 namespace tfb {
 
-enum Method : int { kDirect = 0, kWide = 1, kFast = 2, kRigorous = 3, kKahan = 4 };
+enum Method : int {
+  kDirect = 0, kWide = 1, kFast = 2, kRigorous = 3, kKahan = 4,
+  // opt-in TwoProduct dots (not in the reference, which
+  // rounds every product, kernels.py:23-26): the product's exact round-off
+  // fma(a, b, -fl(a*b)) is added to the error channel.
+  kFastTP = 5, kRigorousTP = 6
+};
+
+// The summation recurrence a method uses (TP variants sum like their base).
+template <int M> struct Base { static constexpr int value = M; };
+template <> struct Base<kFastTP> { static constexpr int value = kFast; };
+template <> struct Base<kRigorousTP> { static constexpr int value = kRigorous; };
+template <int M> __host__ __device__ constexpr bool is_tp() { return M == kFastTP || M == kRigorousTP; }
 
 template <typename T> struct Ar;
 template <> struct Ar<float> {
   static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
   static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
   static __device__ __forceinline__ float mul(float a, float b) { return __fmul_rn(a, b); }
+  static __device__ __forceinline__ float fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 };
 template <> struct Ar<double> {
   static __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
   static __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
   static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+  static __device__ __forceinline__ double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
 };
 
 // (value, error) state.  For KAHAN, `e` holds the pending correction c.
@@ -50,9 +64,10 @@ __device__ __forceinline__ typename Acc<M, T>::type addend(T a, T b) {
 }
 
 // One element of the sequential recurrence.
-template <int M, typename A>
+template <int M0, typename A>
 __device__ __forceinline__ void step(Pair<A>& st, A y) {
   using R = Ar<A>;
+  constexpr int M = Base<M0>::value;
   if constexpr (M == kDirect || M == kWide) {
     st.s = R::add(st.s, y);
   } else if constexpr (M == kFast) {
@@ -76,9 +91,10 @@ __device__ __forceinline__ void step(Pair<A>& st, A y) {
 }
 
 // Merge right state R into left state L (order matters for the error fold).
-template <int M, typename A>
+template <int M0, typename A>
 __device__ __forceinline__ Pair<A> merge(Pair<A> L, Pair<A> Rt) {
   using R = Ar<A>;
+  constexpr int M = Base<M0>::value;
   if constexpr (M == kDirect || M == kWide) {
     L.s = R::add(L.s, Rt.s);
   } else if constexpr (M == kFast || M == kRigorous) {
@@ -98,6 +114,21 @@ __device__ __forceinline__ Pair<A> merge(Pair<A> L, Pair<A> Rt) {
 
 template <typename A>
 __device__ __forceinline__ Pair<A> zero_pair() { return Pair<A>{A(0), A(0)}; }
+
+// One element: the addend through the recurrence; for TP dots also the
+// product's exact round-off r = fma(a, b, -p) into the error channel.
+template <int M, typename T, bool DOT>
+__device__ __forceinline__ void accumulate(Pair<typename Acc<M, T>::type>& st, T a, T b) {
+  using A = typename Acc<M, T>::type;
+  if constexpr (DOT && is_tp<M>()) {
+    const T p = Ar<T>::mul(a, b);
+    const T r = Ar<T>::fma(a, b, -p);
+    step<M, A>(st, p);
+    st.e = Ar<A>::add(st.e, r);
+  } else {
+    step<M, A>(st, addend<M, T, DOT>(a, b));
+  }
+}
 
 // Dekker FAST-TWO-SUM (eft.py:39-42) and Knuth TWO-SUM (eft.py:51-56).
 template <typename T>

@@ -62,7 +62,9 @@ __device__ __forceinline__ Pair<A> ld_pair_cg(const Pair<A>* p) {
   return r;
 }
 
-template <int M> struct HasErr { static constexpr bool value = (M == kFast || M == kRigorous || M == kKahan); };
+template <int M> struct HasErr {
+  static constexpr bool value = (M == kFast || M == kRigorous || M == kKahan || M == kFastTP || M == kRigorousTP);
+};
 
 // Balanced contiguous binary tree over the first `width` (power of two,
 // 1..256) threads' states; result valid in thread 0.  Level `off` merges
@@ -156,13 +158,12 @@ template <int M, typename T, bool DOT, int U>
 __device__ __forceinline__ void consume_batch(Pair<typename Acc<M, T>::type>& st,
                                               const typename Vec<T>::type (&a)[U],
                                               const typename Vec<T>::type (&b)[U]) {
-  using A = typename Acc<M, T>::type;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
 #pragma unroll
     for (int j = 0; j < Vec<T>::V; ++j) {
-      if constexpr (DOT) step<M, A>(st, addend<M, T, true>(vget(a[u], j), vget(b[u], j)));
-      else step<M, A>(st, addend<M, T, false>(vget(a[u], j), T(0)));
+      if constexpr (DOT) accumulate<M, T, true>(st, vget(a[u], j), vget(b[u], j));
+      else accumulate<M, T, false>(st, vget(a[u], j), T(0));
     }
   }
 }
@@ -213,8 +214,8 @@ __device__ __forceinline__ Pair<typename Acc<M, T>::type> leaf_chain(
       if constexpr (DOT) b = ld_stream(yv + static_cast<int64_t>(k) * kThreads);
 #pragma unroll
       for (int j = 0; j < V; ++j) {
-        if constexpr (DOT) step<M, A>(st, addend<M, T, true>(vget(a, j), vget(b, j)));
-        else step<M, A>(st, addend<M, T, false>(vget(a, j), T(0)));
+        if constexpr (DOT) accumulate<M, T, true>(st, vget(a, j), vget(b, j));
+        else accumulate<M, T, false>(st, vget(a, j), T(0));
       }
     }
   } else {
@@ -225,8 +226,7 @@ __device__ __forceinline__ Pair<typename Acc<M, T>::type> leaf_chain(
       for (int j = 0; j < V; ++j) {
         const int64_t i = base + j;
         if (i < n) {
-          if constexpr (DOT) step<M, A>(st, addend<M, T, true>(x[i], y[i]));
-          else step<M, A>(st, addend<M, T, false>(x[i], T(0)));
+          accumulate<M, T, DOT>(st, x[i], DOT ? y[i] : T(0));
         }
       }
     }
@@ -321,13 +321,11 @@ __global__ void seq_kernel(const T* __restrict__ x, const T* __restrict__ y, int
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      if constexpr (DOT) step<M, A>(st, addend<M, T, true>(a[q], b[q]));
-      else step<M, A>(st, addend<M, T, false>(a[q], T(0)));
+      accumulate<M, T, DOT>(st, a[q], DOT ? b[q] : T(0));
     }
   }
   for (; i < n; ++i) {
-    if constexpr (DOT) step<M, A>(st, addend<M, T, true>(x[i], y[i]));
-    else step<M, A>(st, addend<M, T, false>(x[i], T(0)));
+    accumulate<M, T, DOT>(st, x[i], DOT ? y[i] : T(0));
   }
   out[0] = st;
 }
@@ -344,8 +342,7 @@ __global__ void lanes_kernel(const T* __restrict__ x, const T* __restrict__ y, i
   const int64_t nb = n - n % k;
   Pair<A> st = zero_pair<A>();
   for (int64_t i = 0; i < nb; i += k) {
-    if constexpr (DOT) step<M, A>(st, addend<M, T, true>(x[i + j], y[i + j]));
-    else step<M, A>(st, addend<M, T, false>(x[i + j], T(0)));
+    accumulate<M, T, DOT>(st, x[i + j], DOT ? y[i + j] : T(0));
   }
   lane_state[j] = st;
   __syncthreads();
@@ -359,8 +356,7 @@ __global__ void lanes_kernel(const T* __restrict__ x, const T* __restrict__ y, i
     for (int q = 1; q < k; ++q) s = merge<M, A>(s, lane_state[q]);
   }
   for (int64_t i = nb; i < n; ++i) {
-    if constexpr (DOT) step<M, A>(s, addend<M, T, true>(x[i], y[i]));
-    else step<M, A>(s, addend<M, T, false>(x[i], T(0)));
+    accumulate<M, T, DOT>(s, x[i], DOT ? y[i] : T(0));
   }
   out[0] = s;
 }
@@ -503,19 +499,38 @@ static int launch_tree(const void* pairs, int64_t count, void* out, cudaStream_t
                                  else return CALL(kKahan, float, false); }       \
         else { if (dot) return CALL(kKahan, double, true);                       \
                else return CALL(kKahan, double, false); }                        \
+      case kFastTP:                                                              \
+        if (!(dot)) return TF_EINVAL_ARG;                                        \
+        if ((dtype) == TF_F32) return CALL(kFastTP, float, true);                \
+        else return CALL(kFastTP, double, true);                                 \
+      case kRigorousTP:                                                          \
+        if (!(dot)) return TF_EINVAL_ARG;                                        \
+        if ((dtype) == TF_F32) return CALL(kRigorousTP, float, true);            \
+        else return CALL(kRigorousTP, double, true);                             \
       default:                                                                   \
         return TF_EINVAL_METHOD;                                                 \
     }                                                                            \
   } while (0)
 
 static size_t pair_bytes(int method, int dtype) {
-  return (method == TF_WIDE || dtype == TF_F64) ? 16u : 8u;
+  return ((method & ~TF_TRACK_PRODUCT) == TF_WIDE || dtype == TF_F64) ? 16u : 8u;
+}
+
+// Public method id (+ TF_TRACK_PRODUCT flag) -> internal Method id.
+static int internal_method(int method) {
+  const int base = method & ~TF_TRACK_PRODUCT;
+  if (!(method & TF_TRACK_PRODUCT)) return base;
+  if (base == TF_TWOFOLD_FAST) return kFastTP;
+  if (base == TF_TWOFOLD_RIGOROUS) return kRigorousTP;
+  return -1;
 }
 
 static int validate(int method, int dtype) {
-  if (method < TF_DIRECT || method > TF_KAHAN) return TF_EINVAL_METHOD;
+  const int base = method & ~TF_TRACK_PRODUCT;
+  if (base < TF_DIRECT || base > TF_KAHAN) return TF_EINVAL_METHOD;
   if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
-  if (method == TF_WIDE && dtype != TF_F32) return TF_EINVAL_DTYPE;
+  if (base == TF_WIDE && dtype != TF_F32) return TF_EINVAL_DTYPE;
+  if (internal_method(method) < 0) return TF_EINVAL_ARG;  // TwoProduct needs a twofold method
   return TF_OK;
 }
 
@@ -581,7 +596,7 @@ int tf_reduce_rows(int method, int dtype, const void* x, const void* y, int64_t 
   const bool dot = y != nullptr;
 #define TFB_CALL_LEAVES(M, T, DOT) \
   launch_leaves<M, T, DOT>(x, y, ldx, ldy, rows, cols, lg, parts, counters, out_pairs, 1, s)
-  TFB_DISPATCH(method, dtype, dot, TFB_CALL_LEAVES);
+  TFB_DISPATCH(internal_method(method), dtype, dot, TFB_CALL_LEAVES);
 #undef TFB_CALL_LEAVES
 }
 
@@ -606,7 +621,7 @@ int tf_reduce_leaves(int method, int dtype, const void* x, const void* y, int64_
   const bool dot = y != nullptr;
 #define TFB_CALL_PARTS(M, T, DOT) \
   launch_leaves<M, T, DOT>(x, y, n, n, 1, n, lg, partials_out, nullptr, nullptr, 0, s)
-  TFB_DISPATCH(method, dtype, dot, TFB_CALL_PARTS);
+  TFB_DISPATCH(internal_method(method), dtype, dot, TFB_CALL_PARTS);
 #undef TFB_CALL_PARTS
 }
 
@@ -617,7 +632,7 @@ int tf_merge_tree(int method, int dtype, const void* pairs, int64_t count, void*
   if (count < 0) return TF_EINVAL_SHAPE;
   if (!out_pair || (count > 0 && !pairs)) return TF_EINVAL_ARG;
   auto s = static_cast<cudaStream_t>(stream);
-  switch (method) {
+  switch (method & ~TF_TRACK_PRODUCT) {  // TwoProduct pairs merge like their base method
     case TF_DIRECT:
       return dtype == TF_F32 ? launch_tree<kDirect, float>(pairs, count, out_pair, s)
                              : launch_tree<kDirect, double>(pairs, count, out_pair, s);
@@ -644,7 +659,7 @@ int tf_reduce_seq(int method, int dtype, const void* x, const void* y, int64_t n
   auto s = static_cast<cudaStream_t>(stream);
   const bool dot = y != nullptr;
 #define TFB_CALL_SEQ(M, T, DOT) launch_seq<M, T, DOT>(x, y, n, out_pair, s)
-  TFB_DISPATCH(method, dtype, dot, TFB_CALL_SEQ);
+  TFB_DISPATCH(internal_method(method), dtype, dot, TFB_CALL_SEQ);
 #undef TFB_CALL_SEQ
 }
 
@@ -658,7 +673,7 @@ int tf_reduce_lanes(int method, int dtype, const void* x, const void* y, int64_t
   auto s = static_cast<cudaStream_t>(stream);
   const bool dot = y != nullptr;
 #define TFB_CALL_LANES(M, T, DOT) launch_lanes<M, T, DOT>(x, y, n, lanes, out_pair, s)
-  TFB_DISPATCH(method, dtype, dot, TFB_CALL_LANES);
+  TFB_DISPATCH(internal_method(method), dtype, dot, TFB_CALL_LANES);
 #undef TFB_CALL_LANES
 }
 

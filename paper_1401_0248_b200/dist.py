@@ -41,12 +41,13 @@ def shard_range(n: int, rank: int, world: int, leaf_log2: int) -> tuple[int, int
     return min(lo * L, n), min(hi * L, n)
 
 
-def _default_local(method: Method, x: torch.Tensor, y, leaf_log2: int) -> torch.Tensor:
+def _default_local(method: Method, x: torch.Tensor, y, leaf_log2: int, track_product: bool = False) -> torch.Tensor:
     from .api import _device_for, _on_device, _reduce_grid, _reduce_grid_host
     if x.is_cuda:
-        return _reduce_grid(method, x.contiguous(), _on_device(y, x.device), leaf_log2)
+        return _reduce_grid(method, x.contiguous(), _on_device(y, x.device), leaf_log2,
+                            track_product=track_product)
     # host shard: leaf-aligned chunks streamed H2D, overlapped with the leaf kernels
-    return _reduce_grid_host(method, x, y, _device_for(x), leaf_log2)
+    return _reduce_grid_host(method, x, y, _device_for(x), leaf_log2, track_product)
 
 
 def _default_merge(method: Method, pairs: torch.Tensor) -> torch.Tensor:
@@ -61,7 +62,8 @@ def _world(group) -> tuple[int, int]:
 
 def sharded_reduce(method: Method, x_local: torch.Tensor, y_local: torch.Tensor | None = None, *,
                    n_global: int, leaf_log2: int = 0, group=None,
-                   local_reduce: LocalReduce | None = None, merge: Merge | None = None) -> torch.Tensor:
+                   local_reduce: LocalReduce | None = None, merge: Merge | None = None,
+                   track_product: bool = False) -> torch.Tensor:
     """Raw (value, error) pair of the global array, identical on every rank.
 
     x_local / y_local: this rank's shard (CUDA tensors for the default
@@ -69,7 +71,10 @@ def sharded_reduce(method: Method, x_local: torch.Tensor, y_local: torch.Tensor 
     partition does not depend on G.
     """
     lg = leaf_log2 or leaf_log2_for(x_local.dtype, n_global)
-    local = (local_reduce or _default_local)(method, x_local, y_local, lg)
+    if local_reduce is None:
+        local = _default_local(method, x_local, y_local, lg, track_product)
+    else:
+        local = local_reduce(method, x_local, y_local, lg)
     _, world = _world(group)
     if world == 1:
         return local
@@ -80,14 +85,15 @@ def sharded_reduce(method: Method, x_local: torch.Tensor, y_local: torch.Tensor 
 
 
 def sharded_run(method: Method, x_local, y_local=None, *, n_global: int, leaf_log2: int = 0, group=None,
-                local_reduce: LocalReduce | None = None, merge: Merge | None = None) -> SumResult:
+                local_reduce: LocalReduce | None = None, merge: Merge | None = None,
+                track_product: bool = False) -> SumResult:
     """SumResult of the global sum / dot (reference result conventions)."""
     if not isinstance(x_local, torch.Tensor):
         x_local = torch.as_tensor(x_local)
     if y_local is not None and not isinstance(y_local, torch.Tensor):
         y_local = torch.as_tensor(y_local)
     pair = sharded_reduce(method, x_local, y_local, n_global=n_global, leaf_log2=leaf_log2, group=group,
-                          local_reduce=local_reduce, merge=merge)
+                          local_reduce=local_reduce, merge=merge, track_product=track_product)
     v, e = pair.cpu().tolist()
     t = np.float64 if method is Method.WIDE else _np_type(x_local.dtype)
     if method in _TWOFOLD_METHODS:

@@ -297,3 +297,28 @@ def test_exact_integer_data_all_flavors(tfb, dt):
                    tfb.Flavor.vectorized(4), tfb.Flavor.cuda()):
             r = tfb.run_flavor(meth, fl, x)
             assert float(r.value) == 5050.0 and float(r.error) == 0.0, (meth, fl)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_two_product_dot(tfb, oracle, cuda, dt):
+    """Opt-in TwoProduct (TF_TRACK_PRODUCT): bit-exact with the emulator in every flavor,
+    and v+e tracks the exact dot of the TRUE products (rigorous: to ~N eps^2)."""
+    for n in (1, 17, 4097, 100_003, (1 << 20) + 3):
+        xh = oracle.lcg_fill("mmix", n, 31, dt, True)
+        yh = oracle.lcg_fill("nr", n, 32, dt, True)
+        x, y = torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda)
+        for base, m in ((tfb.Method.TWOFOLD_FAST, 5), (tfb.Method.TWOFOLD_RIGOROUS, 6)):
+            got = tfb.reduce(base, x, y, track_product=True).cpu().numpy()
+            _same(got, oracle.emulate(m, xh, yh), (dt, n, m))
+            if n <= 5000:
+                for fl, want in ((tfb.Flavor.sequential(), oracle.seq(m, xh, yh)),
+                                 (tfb.Flavor.unrolled(4), oracle.lanes(m, xh, yh, 4))):
+                    _same(tfb.reduce(base, x, y, flavor=fl, track_product=True).cpu().numpy(), want, (fl, m))
+        if n >= 4097:
+            S, A = oracle.exact_true_dot(xh, yh), oracle.abs_true_dot(xh, yh)
+            r = tfb.dot_twofold_rigorous(x, y, track_product=True)
+            assert oracle.deviation(r.value, r.error, S) <= oracle.bound(3, dt, n, A)
+    with pytest.raises(ValueError):
+        tfb.reduce(tfb.Method.KAHAN, x, y, track_product=True)
+    with pytest.raises(ValueError):
+        tfb.reduce(tfb.Method.TWOFOLD_FAST, x, track_product=True)

@@ -44,10 +44,22 @@ def test_sm100a_code_present(sass):
     assert "sm_100a" in arch
 
 
+def _is_two_product(fn):
+    # internal method ids 5/6 (kFastTP / kRigorousTP) are the opt-in TwoProduct dots
+    return bool(re.search(r"kernelILi[56]E", fn))
+
+
+def test_two_product_kernels_use_fma(sass):
+    tp = [fn for fn in sass if _is_two_product(fn)]
+    assert len(tp) >= 12
+    for fn in tp:
+        assert any(re.search(r"\b(DFMA|FFMA)\b", ln) for ln in sass[fn]), fn
+
+
 def test_no_fused_multiply_add_in_reduction_kernels(sass):
     bad = []
     for fn, lines in sass.items():
-        if any(k in fn for k in REDUCTION):
+        if any(k in fn for k in REDUCTION) and not _is_two_product(fn):
             for ln in lines:
                 if re.search(r"\b(FFMA|DFMA|FFMA2)\b", ln):
                     bad.append((fn, ln.strip()))
