@@ -159,6 +159,28 @@ int tf_fill(int dist, int dtype, uint64_t seed, uint64_t stream_id, uint64_t off
             int64_t n, double p0, double p1, double p2, int64_t total,
             void* out, void* stream);
 
+/* The reference's LCG generators (lcg.py:75-116), bit-identical to
+ * twofold.fill(kind, offset+n, seed, dtype, sym)[offset:]: kind 0 = Numerical
+ * Recipes (32-bit), 1 = MMIX (64-bit); state jump-ahead makes any slice
+ * independent, so the reference's accuracy experiments can run on GPU data. */
+int tf_lcg_fill(int kind, int dtype, uint64_t seed, int sym, int64_t offset, int64_t n,
+                void* out, void* stream);
+
+/* Exact (correctly rounded) sum of addends on the GPU — the device counterpart
+ * of the reference's expansion oracle (expansion.py:79-140).
+ * Addends: x_i (y == NULL); fl_T(x_i*y_i) (the twofold dot kernels' addends);
+ * or, with TF_EXACT_TRUE_PRODUCTS, the exact products x_i*y_i.  TF_EXACT_ABS
+ * sums |addend| instead.  out2 (device, 2 doubles): hi = fl(S), lo = fl(S - hi).
+ * limbs_out (device, optional, 73 int64): S = sum_k limbs[k] 2^(32k-1074) +
+ * limbs[72] 2^(32*72-1074), for exact checks.  Non-finite addends give NaN.
+ * Scratch: records (tf_exact_workspace bytes) + one zeroed uint32 counter (left
+ * zero).  Integer accumulation makes the result independent of the grid. */
+#define TF_EXACT_ABS           1
+#define TF_EXACT_TRUE_PRODUCTS 2
+int tf_exact_workspace(int64_t* records, size_t* bytes);
+int tf_exact(int dtype, const void* x, const void* y, int64_t n, int flags, void* out2,
+             void* limbs_out, void* records, size_t records_bytes, void* counter, void* stream);
+
 /* cfg4 rows: out[r*ld + c] = N(0,1)[stream_id, (row0+r)*cols + c] * 10^U_r with
  * U_r = lo + (hi-lo)*u(seed, scale_stream, row0+r), one scale per row. */
 int tf_fill_rows_scaled(int dtype, uint64_t seed, uint64_t stream_id,

@@ -39,7 +39,8 @@ from .api import (
     workspace_size,
 )
 from .dist import shard_range, sharded_reduce, sharded_run
-from .gen import CONFIGS, make_inputs, philox_fill, rows_scaled_normal
+from .exact import ExactValue, exact_dot, exact_sum, relative_error
+from .gen import CONFIGS, lcg_fill, make_inputs, philox_fill, rows_scaled_normal
 
 __version__ = "0.1.0"
 
@@ -50,6 +51,7 @@ __all__ = [
     "dot_direct", "dot_wide", "dot_twofold_fast", "dot_twofold_rigorous", "dot_kahan",
     "reduce", "reduce_rows", "sum_rows", "dot_rows", "merge_pairs", "workspace_size", "leaf_log2_for",
     "shard_range", "sharded_reduce", "sharded_run",
-    "philox_fill", "rows_scaled_normal", "make_inputs", "CONFIGS",
+    "ExactValue", "exact_sum", "exact_dot", "relative_error",
+    "philox_fill", "lcg_fill", "rows_scaled_normal", "make_inputs", "CONFIGS",
     "__version__",
 ]

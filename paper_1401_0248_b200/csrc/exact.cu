@@ -1,0 +1,328 @@
+// exact.cu — exact (correctly rounded) sum / dot on the GPU: SURVEY.md §8(f) f2,
+// the device counterpart of the reference's expansion oracle
+// (expansion.py:79-140: exact_sum, exact_dot, Expansion.hi/.lo, relative_error).
+//
+// Method (ExBLAS-style, all integer steps exact and associative):
+//   * each thread keeps a K=4-component floating-point expansion; every addend
+//     goes through a TwoSum cascade (exact: the multiset value never changes);
+//     whatever falls out of the last component is deposited into the CTA's
+//     fixed-point superaccumulator in shared memory;
+//   * the superaccumulator anchors bit 0 at 2^-1074 and stores 32-bit digits
+//     in int64 limbs (carry-save; 2^31 deposits per limb before overflow);
+//   * at the end every thread deposits its expansion, the CTA normalises its
+//     limbs and writes one record; the last CTA sums the records as integers
+//     (exact and order-independent, hence bit-reproducible for any grid),
+//     normalises, and rounds to hi = fl(S), lo = fl(S - hi) (round to nearest
+//     even; the reference's relative_error uses exactly these two leading
+//     components, expansion.py:129-140).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "eft.cuh"
+#include "status.h"
+#include "twofold_b200.h"
+
+namespace tfb {
+
+constexpr int kExactThreads = 256;
+constexpr int kLimbs = 72;   // 72 * 32 = 2304 bit positions >= 2098 + 64 carry bits
+constexpr int kExpK = 4;     // per-thread expansion length
+
+// One CTA record: kLimbs normalised digits in [0, 2^32) + a signed top carry,
+// + a non-finite counter.
+struct ExactRecord {
+  long long limb[kLimbs];
+  long long top;
+  long long nonfinite;
+};
+
+__device__ __forceinline__ void deposit(long long* acc, double v) {
+  if (v == 0.0) return;
+  const unsigned long long bits = __double_as_longlong(v);
+  const bool neg = bits >> 63;
+  const int ebits = static_cast<int>((bits >> 52) & 0x7FF);
+  unsigned long long m = bits & 0xFFFFFFFFFFFFFull;
+  int s;  // bit position of the significand's LSB above 2^-1074
+  if (ebits == 0) {
+    s = 0;  // subnormal: m * 2^-1074
+  } else {
+    m |= 1ull << 52;
+    s = ebits - 1;  // normal: m * 2^(ebits - 1075) = m * 2^(ebits-1 - 1074)
+  }
+  const int d = s >> 5, r = s & 31;
+  const unsigned long long lo = m << r;                       // bits 0..63 of m << r
+  const unsigned long long hi = r ? (m >> (64 - r)) : 0ull;    // bits 64..84
+  long long c0 = static_cast<long long>(lo & 0xFFFFFFFFull);
+  long long c1 = static_cast<long long>(lo >> 32);
+  long long c2 = static_cast<long long>(hi);
+  if (neg) { c0 = -c0; c1 = -c1; c2 = -c2; }
+  auto* u = reinterpret_cast<unsigned long long*>(acc);
+  if (c0) atomicAdd(u + d, static_cast<unsigned long long>(c0));
+  if (c1) atomicAdd(u + d + 1, static_cast<unsigned long long>(c1));
+  if (c2) atomicAdd(u + d + 2, static_cast<unsigned long long>(c2));
+}
+
+__device__ __forceinline__ void cascade(double (&a)[kExpK], double x, long long* acc) {
+#pragma unroll
+  for (int i = 0; i < kExpK; ++i) {
+    double s, e;
+    two_sum<double>(a[i], x, s, e);
+    a[i] = s;
+    x = e;
+  }
+  if (x != 0.0) deposit(acc, x);
+}
+
+// Addends: 0 = x_i, 1 = fl_T(x_i*y_i) (the twofold kernels' addends), 2 = exact
+// products (fl(x*y) and fma(x, y, -fl(x*y)) for binary64; exact in binary64 for
+// binary32 data).  abs: |addend| (A = sum |y_i| of the tolerances).
+template <typename T>
+__device__ __forceinline__ void add_element(double (&a)[kExpK], long long* acc, T xv, T yv, int mode,
+                                            bool absval, int& nonfinite) {
+  double p, r = 0.0;
+  if (mode == 0) {
+    p = static_cast<double>(xv);
+  } else if (mode == 1) {
+    p = static_cast<double>(Ar<T>::mul(xv, yv));
+  } else if (sizeof(T) == 4) {
+    p = __dmul_rn(static_cast<double>(xv), static_cast<double>(yv));  // exact
+  } else {
+    p = __dmul_rn(static_cast<double>(xv), static_cast<double>(yv));
+    r = __fma_rn(static_cast<double>(xv), static_cast<double>(yv), -p);
+  }
+  if (!isfinite(p) || !isfinite(r)) {
+    ++nonfinite;
+    return;
+  }
+  if (absval && p < 0.0) {  // |p + r| = -(p + r) when p < 0 (|r| <= ulp(p)/2)
+    p = -p;
+    r = -r;
+  }
+  cascade(a, p, acc);
+  if (r != 0.0) cascade(a, r, acc);
+}
+
+// Normalise limbs (digits -> [0, 2^32), signed carry out) by one thread.
+__device__ void normalise(long long* limb, long long& top) {
+  long long carry = 0;
+  for (int k = 0; k < kLimbs; ++k) {
+    const long long v = limb[k] + carry;  // |v| < 2^63 by the deposit bound
+    limb[k] = v & 0xFFFFFFFFll;
+    carry = v >> 32;                      // arithmetic shift: floor division
+  }
+  top += carry;
+}
+
+// Round the big integer value (sign, magnitude digits) * 2^-1074 to binary64,
+// nearest-even.  mag: kLimbs+2 digits in [0, 2^32).
+__device__ double round_digits(const unsigned long long* mag, int ndig, bool neg) {
+  int hd = ndig - 1;
+  while (hd >= 0 && mag[hd] == 0) --hd;
+  if (hd < 0) return 0.0;
+  const int hb = 63 - __clzll(mag[hd]);      // highest set bit inside digit hd
+  const int p = hd * 32 + hb;                // position of the leading bit
+  auto bit = [&](int q) -> unsigned long long {
+    return q < 0 ? 0ull : (mag[q >> 5] >> (q & 31)) & 1ull;
+  };
+  double out;
+  if (p < 53) {  // exactly representable: integer < 2^53 times 2^-1074
+    unsigned long long m = 0;
+    for (int q = p; q >= 0; --q) m = (m << 1) | bit(q);
+    out = scalbn(static_cast<double>(m), -1074);
+  } else {
+    unsigned long long m = 0;
+    for (int q = p; q > p - 53; --q) m = (m << 1) | bit(q);
+    const int lsb = p - 52;                  // weight of m's last bit
+    const unsigned long long guard = bit(lsb - 1);
+    bool sticky = false;
+    for (int q = lsb - 2; q >= 0 && !sticky; --q) sticky = bit(q);
+    if (guard && (sticky || (m & 1ull))) ++m;  // may carry to 2^53: still exact in scalbn
+    out = scalbn(static_cast<double>(m), lsb - 1074);
+  }
+  return neg ? -out : out;
+}
+
+// Convert normalised (limb, top) to sign + magnitude digits.
+__device__ bool to_magnitude(const long long* limb, long long top, unsigned long long* mag, int ndig) {
+  // value = sum limb_k 2^(32k) + top * 2^(32 kLimbs); top in {.., -1, 0, 1, ..}
+  // put it in two's complement over ndig digits, then negate if negative
+  for (int k = 0; k < ndig; ++k) mag[k] = 0;
+  for (int k = 0; k < kLimbs; ++k) mag[k] = static_cast<unsigned long long>(limb[k]);
+  long long t = top;
+  for (int k = kLimbs; k < ndig; ++k) {
+    mag[k] = static_cast<unsigned long long>(t) & 0xFFFFFFFFull;
+    t >>= 32;
+  }
+  const bool neg = top < 0;
+  if (neg) {  // magnitude = 2^(32 ndig) - value (two's complement negate)
+    unsigned long long borrow = 1;
+    for (int k = 0; k < ndig; ++k) {
+      unsigned long long v = (~mag[k] & 0xFFFFFFFFull) + borrow;
+      mag[k] = v & 0xFFFFFFFFull;
+      borrow = v >> 32;
+    }
+  }
+  return neg;
+}
+
+// One thread: normalise the summed records, round to (hi, lo), emit limbs.
+__device__ __noinline__ void finish(long long* tot, double* out, long long* limbs_out, unsigned* counter) {
+  long long top = tot[kLimbs];
+  const long long nonfin = tot[kLimbs + 1];
+  normalise(tot, top);
+  constexpr int kDig = kLimbs + 2;
+  unsigned long long mag[kDig];
+  const bool neg = to_magnitude(tot, top, mag, kDig);
+  if (limbs_out) {
+    for (int k = 0; k < kLimbs; ++k) limbs_out[k] = tot[k];
+    limbs_out[kLimbs] = top;
+  }
+  if (nonfin) {
+    out[0] = __longlong_as_double(0x7FF8000000000000ll);
+    out[1] = out[0];
+    *counter = 0u;
+    return;
+  }
+  const double hi = round_digits(mag, kDig, neg);
+  if (!isfinite(hi)) {  // |S| beyond binary64: hi = +-inf, no meaningful remainder
+    out[0] = hi;
+    out[1] = 0.0;
+    *counter = 0u;
+    return;
+  }
+  // lo = fl(S - hi): subtract |hi| from the magnitude (same sign), round the rest
+  unsigned long long rem[kDig];
+  for (int k = 0; k < kDig; ++k) rem[k] = mag[k];
+  bool rneg = neg;
+  if (hi != 0.0) {
+    // digits of |hi| * 2^1074
+    unsigned long long hd[kDig];
+    for (int k = 0; k < kDig; ++k) hd[k] = 0;
+    const unsigned long long bits = __double_as_longlong(fabs(hi));
+    const int eb = static_cast<int>(bits >> 52);
+    unsigned long long m = bits & 0xFFFFFFFFFFFFFull;
+    int s = 0;
+    if (eb) { m |= 1ull << 52; s = eb - 1; }
+    const int d = s >> 5, r = s & 31;
+    const unsigned long long lo = m << r, hh = r ? (m >> (64 - r)) : 0ull;
+    if (d < kDig) hd[d] = lo & 0xFFFFFFFFull;
+    if (d + 1 < kDig) hd[d + 1] = lo >> 32;
+    if (d + 2 < kDig) hd[d + 2] = hh;
+    // rem = mag - hd (may go negative: then rem = hd - mag with flipped sign)
+    bool ge = true;
+    for (int k = kDig - 1; k >= 0; --k) {
+      if (rem[k] != hd[k]) { ge = rem[k] > hd[k]; break; }
+    }
+    const unsigned long long* A = ge ? rem : hd;
+    const unsigned long long* B = ge ? hd : rem;
+    unsigned long long diff[kDig];
+    long long borrow = 0;
+    for (int k = 0; k < kDig; ++k) {
+      long long v = static_cast<long long>(A[k]) - static_cast<long long>(B[k]) - borrow;
+      borrow = v < 0;
+      diff[k] = static_cast<unsigned long long>(v + (borrow << 32)) & 0xFFFFFFFFull;
+    }
+    for (int k = 0; k < kDig; ++k) rem[k] = diff[k];
+    rneg = ge ? neg : !neg;
+  }
+  out[0] = hi;
+  out[1] = hi != 0.0 ? round_digits(rem, kDig, rneg) : 0.0;
+  *counter = 0u;  // leave the workspace reusable
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kExactThreads) exact_kernel(
+    const T* __restrict__ x, const T* __restrict__ y, int64_t n, int mode, int absval,
+    ExactRecord* __restrict__ records, unsigned* __restrict__ counter, double* __restrict__ out,
+    long long* __restrict__ limbs_out) {
+  __shared__ long long acc[kLimbs];
+  __shared__ int s_last;
+  __shared__ int s_nonfinite;
+  for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) acc[k] = 0;
+  if (threadIdx.x == 0) s_nonfinite = 0;
+  __syncthreads();
+  double a[kExpK];
+#pragma unroll
+  for (int i = 0; i < kExpK; ++i) a[i] = 0.0;
+  int nonfinite = 0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+    add_element<T>(a, acc, x[i], y ? y[i] : T(0), mode, absval != 0, nonfinite);
+#pragma unroll
+  for (int i = 0; i < kExpK; ++i) deposit(acc, a[i]);
+  if (nonfinite) atomicAdd(&s_nonfinite, nonfinite);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long top = 0;
+    normalise(acc, top);
+    ExactRecord& rec = records[blockIdx.x];
+    for (int k = 0; k < kLimbs; ++k) rec.limb[k] = acc[k];
+    rec.top = top;
+    rec.nonfinite = s_nonfinite;
+    __threadfence();
+    s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // last CTA: integer sum of all records (thread k owns limb k), then finish
+  __shared__ long long tot[kLimbs + 2];
+  for (int k = threadIdx.x; k < kLimbs + 2; k += blockDim.x) {
+    long long v = 0;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      const ExactRecord& rec = records[b];
+      v += k < kLimbs ? __ldcg(&rec.limb[k]) : (k == kLimbs ? __ldcg(&rec.top) : __ldcg(&rec.nonfinite));
+    }
+    tot[k] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  finish(tot, out, limbs_out, counter);
+}
+
+}  // namespace tfb
+
+using namespace tfb;
+
+extern "C" {
+
+int tf_exact_workspace(int64_t* records, size_t* bytes) {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t g = static_cast<int64_t>(sms) * 4;
+  if (records) *records = g;
+  if (bytes) *bytes = static_cast<size_t>(g) * sizeof(ExactRecord);
+  return TF_OK;
+}
+
+int tf_exact(int dtype, const void* x, const void* y, int64_t n, int flags, void* out2,
+             void* limbs_out, void* records, size_t records_bytes, void* counter, void* stream) {
+  if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
+  if (n < 0) return TF_EINVAL_SHAPE;
+  if (!out2 || !counter || (n > 0 && !x)) return TF_EINVAL_ARG;
+  if ((flags & TF_EXACT_TRUE_PRODUCTS) && !y) return TF_EINVAL_ARG;
+  const int mode = y ? ((flags & TF_EXACT_TRUE_PRODUCTS) ? 2 : 1) : 0;
+  int64_t g = 0;
+  size_t need = 0;
+  tf_exact_workspace(&g, &need);
+  const int64_t per = (n + kExactThreads - 1) / kExactThreads;
+  if (g > per && per > 0) g = per;  // tiny inputs: fewer CTAs
+  if (g < 1) g = 1;
+  if (!records || records_bytes < static_cast<size_t>(g) * sizeof(ExactRecord)) return TF_EWORKSPACE;
+  auto s = static_cast<cudaStream_t>(stream);
+  const int absval = (flags & TF_EXACT_ABS) ? 1 : 0;
+  if (dtype == TF_F32)
+    exact_kernel<float><<<static_cast<unsigned>(g), kExactThreads, 0, s>>>(
+        static_cast<const float*>(x), static_cast<const float*>(y), n, mode, absval,
+        static_cast<ExactRecord*>(records), static_cast<unsigned*>(counter), static_cast<double*>(out2),
+        static_cast<long long*>(limbs_out));
+  else
+    exact_kernel<double><<<static_cast<unsigned>(g), kExactThreads, 0, s>>>(
+        static_cast<const double*>(x), static_cast<const double*>(y), n, mode, absval,
+        static_cast<ExactRecord*>(records), static_cast<unsigned*>(counter), static_cast<double*>(out2),
+        static_cast<long long*>(limbs_out));
+  return check_launch();
+}
+
+}  // extern "C"

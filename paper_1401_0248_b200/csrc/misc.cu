@@ -138,6 +138,81 @@ __global__ void fill_rows_scaled_kernel(uint64_t seed, uint64_t sid, uint64_t sc
   }
 }
 
+// ---------------------------------------------------------------------------
+// LCG fills bit-identical to the reference's lcg.fill (lcg.py:75-116), any
+// slice [offset, offset+n) in parallel: s_{i+1} = a s_i + c mod 2^w is an
+// affine map, so the state before element i is reached in O(log i) by
+// composing the precomputed maps T^(2^k) = (A_k, C_k).  Each thread jumps once
+// and then steps through a group of consecutive elements.
+struct LcgJump { uint64_t A[64], C[64]; uint64_t mask; };
+__constant__ LcgJump g_lcg[2];  // 0: Numerical Recipes (w=32), 1: MMIX (w=64)
+
+template <typename T>
+__device__ __forceinline__ T lcg_map(uint64_t s, int kind, int sym);
+template <>
+__device__ __forceinline__ float lcg_map<float>(uint64_t s, int kind, int sym) {
+  // out.dtype.type(s) / scale, then 2v - 1 in the data precision (lcg.py:86-88, :102-104)
+  float v = kind == 0 ? __fmul_rn(__uint2float_rn(static_cast<uint32_t>(s)), 0x1p-32f)
+                      : __fmul_rn(__ull2float_rn(s), 0x1p-64f);
+  return sym ? __fsub_rn(__fmul_rn(2.0f, v), 1.0f) : v;
+}
+template <>
+__device__ __forceinline__ double lcg_map<double>(uint64_t s, int kind, int sym) {
+  double v = kind == 0 ? __dmul_rn(static_cast<double>(static_cast<uint32_t>(s)), 0x1p-32)
+                       : __dmul_rn(__ull2double_rn(s), 0x1p-64);
+  return sym ? __dsub_rn(__dmul_rn(2.0, v), 1.0) : v;
+}
+
+template <typename T>
+__global__ void lcg_fill_kernel(int kind, uint64_t seed, int sym, uint64_t offset, int64_t n,
+                                T* __restrict__ out) {
+  constexpr int G = 8;
+  const LcgJump& J = g_lcg[kind];
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g * G < n;
+       g += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i0 = g * G;
+    // state after (offset + i0) steps: apply T^(offset+i0) to seed
+    uint64_t s = seed & J.mask;
+    uint64_t steps = offset + static_cast<uint64_t>(i0);
+    for (int k = 0; steps; ++k, steps >>= 1)
+      if (steps & 1) s = (J.A[k] * s + J.C[k]) & J.mask;
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      if (i0 + q < n) {
+        s = (J.A[0] * s + J.C[0]) & J.mask;  // fill() advances before it maps
+        out[i0 + q] = lcg_map<T>(s, kind, sym);
+      }
+    }
+  }
+}
+
+static int upload_lcg_tables() {
+  static bool done = false;  // per process; the table is identical on every device
+  static int dev_done = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done && dev_done == dev) return TF_OK;
+  LcgJump t[2];
+  const uint64_t a[2] = {1664525ull, 6364136223846793005ull};
+  const uint64_t c[2] = {1013904223ull, 1442695040888963407ull};
+  const uint64_t mask[2] = {0xFFFFFFFFull, ~0ull};
+  for (int k = 0; k < 2; ++k) {
+    t[k].mask = mask[k];
+    uint64_t A = a[k], C = c[k];
+    for (int b = 0; b < 64; ++b) {
+      t[k].A[b] = A & mask[k];
+      t[k].C[b] = C & mask[k];
+      // T^(2^(b+1)) = T^(2^b) o T^(2^b):  s -> A(As + C) + C
+      C = (A * C + C) & mask[k];
+      A = (A * A) & mask[k];
+    }
+  }
+  if (cudaMemcpyToSymbol(g_lcg, t, sizeof(t)) != cudaSuccess) return record_cuda_error();
+  done = true;
+  dev_done = dev;
+  return TF_OK;
+}
+
 static unsigned grid_for(int64_t n, int threads) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -223,6 +298,25 @@ int tf_fill(int dist, int dtype, uint64_t seed, uint64_t stream_id, uint64_t off
   else
     fill_kernel<double><<<g, 256, 0, s>>>(dist, seed, stream_id, offset, n, p0, p1, p2, total,
                                           static_cast<double*>(out));
+  return check_launch();
+}
+
+int tf_lcg_fill(int kind, int dtype, uint64_t seed, int sym, int64_t offset, int64_t n, void* out,
+                void* stream) {
+  if (kind != 0 && kind != 1) return TF_EINVAL_ARG;
+  if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
+  if (n < 0 || offset < 0) return TF_EINVAL_SHAPE;
+  if (n == 0) return TF_OK;
+  if (!out) return TF_EINVAL_ARG;
+  if (int rc = upload_lcg_tables()) return rc;
+  auto s = static_cast<cudaStream_t>(stream);
+  const unsigned g = grid_for((n + 7) / 8, 256);
+  if (dtype == TF_F32)
+    lcg_fill_kernel<float><<<g, 256, 0, s>>>(kind, seed, sym, static_cast<uint64_t>(offset), n,
+                                             static_cast<float*>(out));
+  else
+    lcg_fill_kernel<double><<<g, 256, 0, s>>>(kind, seed, sym, static_cast<uint64_t>(offset), n,
+                                              static_cast<double*>(out));
   return check_launch();
 }
 

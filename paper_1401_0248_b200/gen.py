@@ -45,6 +45,22 @@ def philox_fill(dist: str, n: int, *, seed: int, stream: int = 0, offset: int = 
     return out
 
 
+def lcg_fill(kind: str, n: int, seed: int = 1, dtype: torch.dtype = torch.float64, sym: bool = False, *,
+             offset: int = 0, device=None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """The reference's LCG data on the device, bit-identical to
+    twofold.fill(LcgKind(kind), offset + n, seed, dtype, sym)[offset:] (lcg.py:108-116).
+    kind: "nr" (Numerical Recipes, 32-bit) or "mmix" (64-bit)."""
+    if kind not in ("nr", "mmix"):
+        raise ValueError(f"unknown LCG kind {kind!r}")
+    dev = _dev(device)
+    if out is None:
+        out = torch.empty(n, dtype=dtype, device=dev)
+    code = _lib.TF_F32 if out.dtype == torch.float32 else _lib.TF_F64
+    check(lib().tf_lcg_fill(0 if kind == "nr" else 1, code, seed, 1 if sym else 0, offset, n, out.data_ptr(),
+                            torch.cuda.current_stream(dev).cuda_stream), "tf_lcg_fill")
+    return out
+
+
 def rows_scaled_normal(rows: int, cols: int, *, seed: int, stream: int, scale_stream: int = 2,
                        row0: int = 0, lo: float = -4.0, hi: float = 4.0,
                        dtype: torch.dtype = torch.float32, device=None) -> torch.Tensor:

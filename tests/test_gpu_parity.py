@@ -322,3 +322,86 @@ def test_two_product_dot(tfb, oracle, cuda, dt):
         tfb.reduce(tfb.Method.KAHAN, x, y, track_product=True)
     with pytest.raises(ValueError):
         tfb.reduce(tfb.Method.TWOFOLD_FAST, x, track_product=True)
+
+
+def test_device_lcg_fill_matches_reference_fill(tfb, oracle, golden):
+    """tf_lcg_fill == lcg.fill bit for bit (golden sha256 of the reference's own
+    arrays), for whole arrays and arbitrary slices (jump-ahead)."""
+    from golden_inputs import sha
+    for key, pin in golden["lcg"].items():
+        kind, dt, interval = key.split("_")
+        tdt = torch.float32 if dt == "f32" else torch.float64
+        d = tfb.lcg_fill(kind, pin["n"], pin["seed"], tdt, interval == "sym").cpu().numpy()
+        assert sha(d) == pin["sha256"], key
+    for kind in ("nr", "mmix"):
+        for tdt, ndt in ((torch.float32, np.float32), (torch.float64, np.float64)):
+            full = oracle.lcg_fill(kind, 200_000, 7, ndt, True)
+            for off, cnt in ((0, 200_000), (1, 99), (12_345, 100_000), (199_990, 10)):
+                d = tfb.lcg_fill(kind, cnt, 7, tdt, True, offset=off).cpu().numpy()
+                assert d.tobytes() == full[off:off + cnt].tobytes(), (kind, tdt, off)
+
+
+def test_gpu_exact_sum_matches_expansion_oracle(tfb, oracle, golden, cuda):
+    """tf_exact == the reference's exact_sum (golden components) and the C
+    expansion oracle, as rationals; hi/lo are the correctly rounded leading parts."""
+    from fractions import Fraction
+    inputs = load_inputs(oracle, golden)
+    for name, rec in golden["inputs"].items():
+        x, y = inputs[name]
+        ref = sum((Fraction(float.fromhex(c)) for c in rec["exact"]), Fraction(0))
+        got = tfb.exact_sum(x) if y is None else tfb.exact_dot(x, y)
+        assert got.fraction() == ref, name
+        assert got.hi == float(ref) if ref else got.hi == 0.0
+        if ref:
+            assert got.lo == float(ref - Fraction(got.hi)), name
+
+
+def test_gpu_exact_hard_cases(tfb, oracle, cuda):
+    from fractions import Fraction
+    rng = np.random.default_rng(3)
+    cases = [
+        np.array([5e-324, 5e-324, -1e-320, 2.0 ** -1022]),            # subnormals
+        np.array([1e308, -1e308, 1e-308, 3.0, -3.0]),                 # extreme exponents
+        np.array([2.0 ** 53, 1.0, -(2.0 ** 53), 2.0 ** -60]),         # ties / cancellation
+        rng.standard_normal(100_003) * 2.0 ** rng.integers(-600, 600, 100_003),
+        oracle.philox_fill("illcond", 1 << 20, 2, 0, total=1 << 20),  # cfg3 layout
+    ]
+    for x in cases:
+        want = sum((Fraction(float(v)) for v in x), Fraction(0)) if len(x) < 1000 else oracle.exact(x)
+        got = tfb.exact_sum(x)
+        assert got.fraction() == want
+        assert got.hi == float(want)
+        a = tfb.exact_sum(x, absolute=True)
+        assert a.fraction() == (sum((abs(Fraction(float(v))) for v in x), Fraction(0)) if len(x) < 1000
+                                else oracle.abs_sum(x))
+    xf = oracle.lcg_fill("mmix", 300_001, 4, np.float32, True)
+    yf = oracle.lcg_fill("nr", 300_001, 5, np.float32, True)
+    assert tfb.exact_dot(xf, yf).fraction() == oracle.exact(xf, yf)
+    assert tfb.exact_dot(xf, yf, true_products=True).fraction() == oracle.exact_true_dot(xf, yf)
+    xd = oracle.lcg_fill("mmix", 300_001, 4, np.float64, True)
+    yd = oracle.lcg_fill("nr", 300_001, 5, np.float64, True)
+    assert tfb.exact_dot(xd, yd, true_products=True).fraction() == oracle.exact_true_dot(xd, yd)
+    assert np.isnan(tfb.exact_sum(np.array([1.0, np.inf])).hi)
+    # grid independence: a slice reduced in place == its copy
+    xt = torch.from_numpy(xd).to(cuda)
+    assert tfb.exact_sum(xt[1:]).fraction() == tfb.exact_sum(xt[1:].clone()).fraction()
+
+
+def test_cfg5_accuracy_at_full_scale_on_gpu(tfb, cuda):
+    """BASELINE cfg5 (f64 dottf, N=2^32) is too large for the CPU oracle in a test;
+    the GPU exact dot checks the twofold result at full size (64 GiB resident)."""
+    from fractions import Fraction
+    free, _ = torch.cuda.mem_get_info()
+    n = 1 << 32 if free > 80 * 2**30 else 1 << 30
+    x = tfb.philox_fill("uniform_sym", n, seed=4, stream=0)
+    y = tfb.philox_fill("uniform_sym", n, seed=4, stream=1)
+    r = tfb.dot_twofold_fast(x, y)
+    S = tfb.exact_dot(x, y).fraction()
+    A = tfb.exact_dot(x, y, absolute=True).fraction()
+    eps = Fraction(2.0 ** -53)
+    D = abs(Fraction(float(r.value)) + Fraction(float(r.error)) - S)
+    assert D <= 2 * n * eps * eps * A + Fraction(1, 64) * eps * A
+    rr = tfb.dot_twofold_rigorous(x, y)
+    assert abs(Fraction(float(rr.value)) + Fraction(float(rr.error)) - S) <= 2 * n * eps * eps * A
+    del x, y
+    torch.cuda.empty_cache()
