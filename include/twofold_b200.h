@@ -145,6 +145,15 @@ int tf_reduce_seq(int method, int dtype, const void* x, const void* y, int64_t n
 int tf_reduce_lanes(int method, int dtype, const void* x, const void* y, int64_t n,
                     int lanes, void* out_pair, void* stream);
 
+/* "noread" compute roof (the paper's p-functions): `blocks`
+ * CTAs of 256 threads each run the method's per-element recurrence over
+ * iters*8 register-resident addends (dot: products of register operands);
+ * seed8 = 8 device values of the data type; out_pairs: blocks*256 pairs.
+ * Throughput = blocks*256*iters*8 / time: the FP ceiling the memory-bound
+ * kernels are compared against (bench.py:281-307 methodology). */
+int tf_noread(int method, int dtype, int dot, const void* seed8, int64_t iters, int64_t blocks,
+              void* out_pairs, void* stream);
+
 /* Elementwise EFTs on device arrays: kind 0 = fast_two_sum (eft.py:28-42),
  * kind 1 = two_sum (eft.py:45-56).  x_out = fl(a+b), y_out = round-off. */
 int tf_eft(int kind, int dtype, const void* a, const void* b, int64_t n,

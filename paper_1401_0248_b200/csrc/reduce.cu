@@ -361,6 +361,29 @@ __global__ void lanes_kernel(const T* __restrict__ x, const T* __restrict__ y, i
   out[0] = s;
 }
 
+// "noread" compute roof (the paper's p-functions; bench.py
+// run_noread_baseline :281-307): the same per-thread recurrence as the grid
+// kernel, fed from registers instead of memory, iters*8 addends per thread.
+// The operands are runtime values and every op is an IEEE intrinsic, so the
+// compiler cannot shorten the chain; the final states are stored to keep it live.
+template <int M, typename T, bool DOT>
+__global__ void __launch_bounds__(kThreads) noread_kernel(const T* __restrict__ seed8, int64_t iters,
+                                                          Pair<typename Acc<M, T>::type>* __restrict__ out) {
+  using A = typename Acc<M, T>::type;
+  T a[8], b[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    a[j] = seed8[j] * static_cast<T>(1 + ((threadIdx.x + j) & 7));
+    b[j] = seed8[(j + 3) & 7];
+  }
+  Pair<A> st = zero_pair<A>();
+  for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) accumulate<M, T, DOT>(st, a[j], DOT ? b[j] : T(0));
+  }
+  out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = st;
+}
+
 // ---------------------------------------------------------------------------
 // Host side.
 
@@ -459,6 +482,14 @@ static int launch_lanes(const void* x, const void* y, int64_t n, int k, void* ou
   using A = typename Acc<M, T>::type;
   lanes_kernel<M, T, DOT><<<1, k, 0, s>>>(static_cast<const T*>(x), static_cast<const T*>(y), n, k,
                                           static_cast<Pair<A>*>(out));
+  return check_launch();
+}
+
+template <int M, typename T, bool DOT>
+static int launch_noread(const void* seed8, int64_t iters, int64_t blocks, void* out, cudaStream_t s) {
+  using A = typename Acc<M, T>::type;
+  noread_kernel<M, T, DOT><<<static_cast<unsigned>(blocks), kThreads, 0, s>>>(
+      static_cast<const T*>(seed8), iters, static_cast<Pair<A>*>(out));
   return check_launch();
 }
 
@@ -648,6 +679,17 @@ int tf_merge_tree(int method, int dtype, const void* pairs, int64_t count, void*
       return dtype == TF_F32 ? launch_tree<kKahan, float>(pairs, count, out_pair, s)
                              : launch_tree<kKahan, double>(pairs, count, out_pair, s);
   }
+}
+
+int tf_noread(int method, int dtype, int dot, const void* seed8, int64_t iters, int64_t blocks,
+              void* out_pairs, void* stream) {
+  int rc = validate(method, dtype);
+  if (rc) return rc;
+  if (iters < 0 || blocks < 1 || !seed8 || !out_pairs) return TF_EINVAL_ARG;
+  auto s = static_cast<cudaStream_t>(stream);
+#define TFB_CALL_NOREAD(M, T, DOT) launch_noread<M, T, DOT>(seed8, iters, blocks, out_pairs, s)
+  TFB_DISPATCH(internal_method(method), dtype, dot != 0, TFB_CALL_NOREAD);
+#undef TFB_CALL_NOREAD
 }
 
 int tf_reduce_seq(int method, int dtype, const void* x, const void* y, int64_t n, void* out_pair,

@@ -1,0 +1,69 @@
+"""The reference's harness experiments on the GPU path (accuracy.py, bench.py
+methodology; test_acceptance.py criteria C1, C4, C5, C7 adapted to the grid flavor)."""
+
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def H(cuda):
+    from paper_1401_0248_b200 import harness
+    return harness
+
+
+def test_hours100_seq_goldens_and_grid(H):
+    """C1 (test_acceptance.py:46-60): the seq flavor reproduces the goldens on the GPU."""
+    import paper_1401_0248_b200 as tfb
+    rows = {r.method: r for r in H.run_hours100(tfb.Flavor.sequential())}
+    assert abs(rows["direct"].result_hours - 96.3958) <= 0.0005
+    assert rows["kahan"].deviation_hours < 1e-5
+    assert rows["wide"].deviation_hours <= 1.5e-6
+    assert abs(rows["twofold-fast"].result_hours - 99.9359) <= 0.001
+    assert abs(rows["twofold-fast"].estimate_hours - 3.54008) <= 0.01
+    grid = {r.method: r for r in H.run_hours100(tfb.Flavor.cuda())}
+    assert grid["twofold-fast"].deviation_hours <= 1.5e-6 and grid["kahan"].deviation_hours < 1e-5
+
+
+def test_accuracy_bands_grid_flavor(H):
+    """C4 (test_acceptance.py:133-164) upper bands on the grid flavor (a tree sum is
+    more accurate than sequential, so the direct lower band does not apply)."""
+    import paper_1401_0248_b200 as tfb
+    rows = H.run_accuracy_table(n=1_000_000)
+    for r in rows:
+        if r.precision == "f32":
+            limit = {"direct": 1e-3, "kahan": 1e-7, "twofold-fast": 1e-9}[r.method]
+            assert abs(r.rel_error) <= limit, r
+    # binary64: value + error within 1e-30 of the exact sum, judged in rationals
+    for gen in ("nr", "mmix"):
+        x = tfb.lcg_fill(gen, 1_000_000, 1, torch.float64)
+        ref = tfb.exact_sum(x).fraction()
+        r = tfb.sum_twofold_fast(x)
+        assert abs((Fraction(float(r.value)) + Fraction(float(r.error)) - ref) / ref) <= Fraction(1, 10 ** 30)
+
+
+def test_scaling_twofold_beats_direct(H):
+    """C5 spirit (test_acceptance.py:167-177): twofold >= 10x better than direct at every n >= 1e4."""
+    pts, slopes = H.run_scaling_study(ns=(10 ** 4, 10 ** 5, 10 ** 6), trials=10)
+    by = {(n, m): e for n, m, e in pts}
+    for n in (10 ** 4, 10 ** 5, 10 ** 6):
+        assert by[(n, "twofold-fast")] <= by[(n, "direct")] / 10
+
+
+def test_table1_orderings(H):
+    """C7 orderings (test_acceptance.py:207-240): noread direct/fast and direct/rigorous
+    ratios, and twofold at the read roof when memory-bound (the paper's thesis)."""
+    mem = H.memory_rows(tiers=("large",), reps=5)
+    nr = H.noread_rows(iters=1024, reps=3)
+    cell = {(r.name, r.precision, r.tier): r.gelem_s for r in mem + nr}
+    for p in ("f32", "f64"):
+        assert 2 <= cell[("psum", p, "noread")] / cell[("psumtf", p, "noread")] <= 6
+        assert 4 <= cell[("psum", p, "noread")] / cell[("psumt", p, "noread")] <= 10
+        for name in ("sumtf", "sumt", "sumk"):
+            assert cell[(name, p, "large")] >= 0.9 * cell[("sum", p, "large")], (name, p)
+        for name in ("dottf", "dott", "dotk"):
+            assert cell[(name, p, "large")] >= 0.9 * cell[("dot", p, "large")], (name, p)
