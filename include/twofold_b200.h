@@ -93,6 +93,11 @@ int tf_canary(void);
  * A pure function of (dtype, n): results never depend on the SM count. */
 int tf_leaf_log2(int dtype, int64_t n);
 
+/* Tuning knob (process-wide): split every leaf's 256 chains over `split`
+ * CTAs (1, 2 or 4; 0 = automatic, the default; env TFB_SPLIT sets the initial
+ * value).  Result-neutral by construction: only the grid balance changes. */
+int tf_set_leaf_split(int split);
+
 /* Scratch for rows x cols (1-D: rows = 1, cols = n) at leaf_log2 (0 = auto):
  *   partials: rows * leaves(cols) (value, error) pairs, any contents on entry;
  *   counters: `rows` uint32 retire-tickets, ZERO on entry and left zero on exit

@@ -296,10 +296,8 @@ def _reduce_grid(method: Method, x: torch.Tensor, y: torch.Tensor | None, leaf_l
     if out is None:
         out = torch.empty(2, dtype=acc, device=dev)
     n = x.numel()
-    pb, cnt, leaves = workspace_size(method, x.dtype, 1, n, leaf_log2)
-    parts = ctrs = None
-    if leaves > 1:
-        parts, ctrs = _scratch.get(dev, pb, cnt)
+    pb, cnt, _ = workspace_size(method, x.dtype, 1, n, leaf_log2)
+    parts, ctrs = _scratch.get(dev, pb, cnt)  # cached per stream; also feeds leaf splitting
     check(lib().tf_reduce(_mid(method, track_product, y is not None), _dtype_code(x.dtype), _ptr(x), _ptr(y), n,
                           leaf_log2,
                           out.data_ptr(), _ptr(parts), pb, _ptr(ctrs), cnt, _stream_ptr(dev)),
@@ -554,10 +552,8 @@ def reduce_rows(method: Method, X, Y=None, *, leaf_log2: int = 0,
     acc = _acc_dtype(method, x.dtype)
     if out is None:
         out = torch.empty(rows, 2, dtype=acc, device=dev)
-    pb, cnt, leaves = workspace_size(method, x.dtype, rows, cols, leaf_log2)
-    parts = ctrs = None
-    if leaves > 1:
-        parts, ctrs = _scratch.get(dev, pb, cnt)
+    pb, cnt, _ = workspace_size(method, x.dtype, rows, cols, leaf_log2)
+    parts, ctrs = _scratch.get(dev, pb, cnt)
     check(lib().tf_reduce_rows(mid, _dtype_code(x.dtype), _ptr(x), _ptr(y), rows, cols,
                                x.stride(0), 0 if y is None else y.stride(0), leaf_log2, out.data_ptr(),
                                _ptr(parts), pb, _ptr(ctrs), cnt, _stream_ptr(dev)), "tf_reduce_rows")

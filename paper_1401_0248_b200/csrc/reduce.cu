@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -28,7 +30,7 @@
 
 namespace tfb {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;  // chains per leaf (the tree geometry) and default CTA size
 constexpr int kWarps = kThreads / 32;
 
 template <typename T> struct Vec;
@@ -60,6 +62,31 @@ __device__ __forceinline__ Pair<A> ld_pair_cg(const Pair<A>* p) {
   r.s = __ldcg(&p->s);
   r.e = __ldcg(&p->e);
   return r;
+}
+
+// Retire ticket: publish this CTA's unit pair (written by the same thread just
+// before) and count it.  TFB_RETIRE_ACQREL=1: one acq_rel RMW at gpu scope;
+// 0: the classic __threadfence + atomicAdd.  The last CTA then runs
+// acquire_fence() before any thread reads the other CTAs' pairs.
+#ifndef TFB_RETIRE_ACQREL
+#define TFB_RETIRE_ACQREL 0  // both forms compile to MEMBAR.ALL.GPU + ATOM + CCTL.IVALL on sm_100a
+#endif
+__device__ __forceinline__ unsigned retire_ticket(unsigned* counter) {
+#if TFB_RETIRE_ACQREL
+  unsigned prev;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(counter) : "memory");
+  return prev;
+#else
+  __threadfence();
+  return atomicAdd(counter, 1u);
+#endif
+}
+__device__ __forceinline__ void acquire_fence() {
+#if TFB_RETIRE_ACQREL
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#else
+  __threadfence();
+#endif
 }
 
 template <int M> struct HasErr {
@@ -108,13 +135,13 @@ __device__ __forceinline__ Pair<A> block_tree(Pair<A> st, Pair<A>* smem, int wid
 // CTA.  If P2 >= 256, thread t first folds leaves [t*g, (t+1)*g), g = P2/256,
 // with a binary-counter stack (the same balanced shape, sequentially), then
 // the 256-thread tree finishes; otherwise threads < P2 hold one pair each.
-template <int M, typename A>
+template <int M, typename A, int NT = kThreads>
 __device__ Pair<A> tree_over(const Pair<A>* parts, int64_t P, Pair<A>* smem) {
   int64_t P2 = 1;
   while (P2 < P) P2 <<= 1;
   const int t = threadIdx.x;
-  if (P2 >= kThreads) {
-    const int64_t g = P2 / kThreads;
+  if (P2 >= NT) {
+    const int64_t g = P2 / NT;
     const int64_t base = static_cast<int64_t>(t) * g;
     Pair<A> stack[32];
     for (int64_t i0 = 0; i0 < g; i0 += 8) {
@@ -137,7 +164,7 @@ __device__ Pair<A> tree_over(const Pair<A>* parts, int64_t P, Pair<A>* smem) {
     }
     int lg = 0;
     while ((int64_t(1) << lg) < g) ++lg;
-    return block_tree<M, A>(stack[lg], smem, kThreads);
+    return block_tree<M, A>(stack[lg], smem, NT);
   }
   Pair<A> cur = t < P ? ld_pair_cg(parts + t) : zero_pair<A>();
   return block_tree<M, A>(cur, smem, static_cast<int>(P2));
@@ -172,12 +199,11 @@ __device__ __forceinline__ void consume_batch(Pair<typename Acc<M, T>::type>& st
 // `start` of a row of n elements.  VEC: 16-byte aligned row, full leaf.
 template <int M, typename T, bool DOT, bool VEC, int U>
 __device__ __forceinline__ Pair<typename Acc<M, T>::type> leaf_chain(
-    const T* __restrict__ x, const T* __restrict__ y, int64_t start, int64_t n, int R) {
+    const T* __restrict__ x, const T* __restrict__ y, int64_t start, int64_t n, int R, int t) {
   using A = typename Acc<M, T>::type;
   using VT = typename Vec<T>::type;
   constexpr int V = Vec<T>::V;
   Pair<A> st = zero_pair<A>();
-  const int t = threadIdx.x;
   const int64_t L = static_cast<int64_t>(R) * kThreads * V;
   if (VEC && start + L <= n) {
     const VT* xv = reinterpret_cast<const VT*>(x + start) + t;
@@ -247,47 +273,54 @@ template <typename T> struct Unroll;
 template <> struct Unroll<float> { static constexpr int value = TFB_UNROLL_F32; };
 template <> struct Unroll<double> { static constexpr int value = TFB_UNROLL_F64; };
 
-// Grid reduction over rows x cols.  Unit u = (row r, leaf l), u = r*P + l.
-// mode 0: write leaf pairs to partials[u] only.  mode 1: fused — the CTA that
-// retires a row's last leaf builds the row tree into out[r].
-template <int M, typename T, bool DOT, bool VEC>
-__global__ void __launch_bounds__(kThreads) leaves_kernel(
+// Grid reduction over rows x cols.  A leaf's 256 chains may be split over
+// S = 256/NT CTAs: unit u = (row r, leaf l, part s), u = (r*P + l)*S + s, and CTA
+// part s runs chains [s*NT, (s+1)*NT).  Its block tree is exactly the leaf
+// tree's subtree over those chains, and the row tree over the P*S unit pairs is
+// the same balanced tree (zero pairs merge to zero pairs), so the result does
+// not depend on S — S only balances the grid over the SMs.
+// mode 0: write unit pairs to partials[u] only.  mode 1: fused — the CTA that
+// retires a row's last unit builds the row tree into out[r].
+template <int M, typename T, bool DOT, bool VEC, int NT>
+__global__ void __launch_bounds__(NT) leaves_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy,
     int64_t rows, int64_t cols, int leaf_log2, int64_t P,
     Pair<typename Acc<M, T>::type>* __restrict__ partials, unsigned* __restrict__ counters,
     Pair<typename Acc<M, T>::type>* __restrict__ out, int fused) {
   using A = typename Acc<M, T>::type;
   constexpr int V = Vec<T>::V;
+  constexpr int S = kThreads / NT;
   __shared__ Pair<A> smem[kWarps];
   __shared__ int s_last;
   const int R = (1 << leaf_log2) / (kThreads * V);
-  const int64_t units = rows * P;
+  const int64_t per_row = P * S;
+  const int64_t units = rows * per_row;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-    const int64_t r = u / P;
-    const int64_t l = u - r * P;
+    const int64_t r = u / per_row;
+    const int64_t rem = u - r * per_row;
+    const int64_t l = rem / S;
+    const int part = static_cast<int>(rem - l * S);
     const T* xr = x + r * ldx;
     const T* yr = DOT ? y + r * ldy : nullptr;
     Pair<A> st = leaf_chain<M, T, DOT, VEC, Unroll<T>::value>(
-        xr, yr, l << leaf_log2, cols, R);
-    st = block_tree<M, A>(st, smem, kThreads);
+        xr, yr, l << leaf_log2, cols, R, part * NT + static_cast<int>(threadIdx.x));
+    st = block_tree<M, A>(st, smem, NT);
     if (!fused) {
       if (threadIdx.x == 0) partials[u] = st;
       continue;
     }
-    if (P == 1) {
+    if (per_row == 1) {
       if (threadIdx.x == 0) out[r] = st;
       continue;
     }
     if (threadIdx.x == 0) {
       partials[u] = st;
-      __threadfence();
-      const unsigned prev = atomicAdd(&counters[r], 1u);
-      s_last = (prev == static_cast<unsigned>(P - 1));
+      s_last = (retire_ticket(&counters[r]) == static_cast<unsigned>(per_row - 1));
     }
     __syncthreads();
     if (s_last) {
-      __threadfence();
-      Pair<A> root = tree_over<M, A>(partials + r * P, P, smem);
+      acquire_fence();
+      Pair<A> root = tree_over<M, A, NT>(partials + r * per_row, per_row, smem);
       if (threadIdx.x == 0) {
         out[r] = root;
         counters[r] = 0u;  // leave the workspace reusable
@@ -403,14 +436,14 @@ static int device_sms() {
   return sms;
 }
 
-static int occupancy_of(const void* fn) {
+static int occupancy_of(const void* fn, int threads = kThreads) {
   static std::mutex mu;
   static std::unordered_map<const void*, int> cache;
   std::lock_guard<std::mutex> g(mu);
   auto it = cache.find(fn);
   if (it != cache.end()) return it->second;
   int blocks = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kThreads, 0) != cudaSuccess ||
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, threads, 0) != cudaSuccess ||
       blocks < 1)
     blocks = 1;
   cache[fn] = blocks;
@@ -440,33 +473,70 @@ int auto_leaf_log2(int dtype, int64_t total) {
   return l;
 }
 
+// Leaf split S = 256/NT for the fused kernel (grid balance for small unit
+// counts).  Result-neutral (see leaves_kernel); TFB_SPLIT=1|2|4 or
+// tf_set_leaf_split() override it.
+constexpr int kMaxSplit = 4;
+static int g_split_override = -1;  // -1: read TFB_SPLIT once; 0: auto; 1|2|4: forced
+
+static int choose_split(int64_t units, int fused) {
+  if (!fused) return 1;  // leaves-only mode promises one pair per leaf
+  if (g_split_override < 0) {
+    const char* e = getenv("TFB_SPLIT");
+    g_split_override = e ? atoi(e) : 0;
+  }
+  const int env = g_split_override;
+  if (env == 1 || env == 2 || env == 4) return env;
+  // measured (profiles/r01_summary.md): with correct scratch the split only
+  // adds unit pairs to the final tree — no grid size benefits, so default off
+  (void)units;
+  return 1;
+}
+
+template <int M, typename T, bool DOT, bool VEC, int NT>
+static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
+                            int leaf_log2, int64_t P, void* partials, void* counters, void* out, int fused,
+                            cudaStream_t stream) {
+  using A = typename Acc<M, T>::type;
+  const void* fn = reinterpret_cast<const void*>(&leaves_kernel<M, T, DOT, VEC, NT>);
+  const int64_t units = rows * P * (kThreads / NT);
+  const int64_t slots = static_cast<int64_t>(device_sms()) * occupancy_of(fn, NT);
+  const int64_t grid64 = units < slots ? units : slots;
+  const unsigned grid = static_cast<unsigned>(grid64 > 0 ? grid64 : 1);
+  leaves_kernel<M, T, DOT, VEC, NT><<<grid, NT, 0, stream>>>(
+      px, py, ldx, ldy, rows, cols, leaf_log2, P, static_cast<Pair<A>*>(partials),
+      static_cast<unsigned*>(counters), static_cast<Pair<A>*>(out), fused);
+  return check_launch();
+}
+
 template <int M, typename T, bool DOT>
 static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy, int64_t rows,
                          int64_t cols, int leaf_log2, void* partials, void* counters, void* out,
-                         int fused, cudaStream_t stream) {
-  using A = typename Acc<M, T>::type;
+                         int fused, cudaStream_t stream, int64_t partial_capacity = -1,
+                         int64_t counter_capacity = -1) {
   const int64_t P = (cols + (int64_t(1) << leaf_log2) - 1) >> leaf_log2;
   const int64_t units = rows * P;
   if (units == 0) return TF_OK;
   const bool vec = aligned16(x) && ((ldx * int64_t(sizeof(T))) % 16 == 0 || rows == 1) &&
                    (!DOT || (aligned16(y) && ((ldy * int64_t(sizeof(T))) % 16 == 0 || rows == 1)));
-  const void* fn = vec ? reinterpret_cast<const void*>(&leaves_kernel<M, T, DOT, true>)
-                       : reinterpret_cast<const void*>(&leaves_kernel<M, T, DOT, false>);
-  const int64_t slots = static_cast<int64_t>(device_sms()) * occupancy_of(fn);
-  const int64_t grid64 = units < slots ? units : slots;
-  const unsigned grid = static_cast<unsigned>(grid64 > 0 ? grid64 : 1);
   auto px = static_cast<const T*>(x);
   auto py = static_cast<const T*>(y);
-  auto pp = static_cast<Pair<A>*>(partials);
-  auto pc = static_cast<unsigned*>(counters);
-  auto po = static_cast<Pair<A>*>(out);
-  if (vec)
-    leaves_kernel<M, T, DOT, true><<<grid, kThreads, 0, stream>>>(px, py, ldx, ldy, rows, cols,
-                                                                   leaf_log2, P, pp, pc, po, fused);
-  else
-    leaves_kernel<M, T, DOT, false><<<grid, kThreads, 0, stream>>>(px, py, ldx, ldy, rows, cols,
-                                                                    leaf_log2, P, pp, pc, po, fused);
-  return check_launch();
+  int S = choose_split(units, fused);
+  // never exceed the scratch the caller provided (fused mode): S unit pairs per leaf
+  // need rows*P*S partials, and any S*P > 1 needs the retire counters
+  if (fused) {
+    while (S > 1 && (partial_capacity < units * S || !partials || !counters || counter_capacity < rows)) S /= 2;
+  }
+
+#define TFB_NT(NT)                                                                                     \
+  (vec ? launch_leaves_nt<M, T, DOT, true, NT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,   \
+                                               counters, out, fused, stream)                          \
+       : launch_leaves_nt<M, T, DOT, false, NT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,  \
+                                                counters, out, fused, stream))
+  if (S == 4) return TFB_NT(64);
+  if (S == 2) return TFB_NT(128);
+  return TFB_NT(256);
+#undef TFB_NT
 }
 
 template <int M, typename T, bool DOT>
@@ -581,6 +651,12 @@ using namespace tfb;
 
 extern "C" {
 
+int tf_set_leaf_split(int split) {
+  if (split != 0 && split != 1 && split != 2 && split != 4) return TF_EINVAL_ARG;
+  g_split_override = split;
+  return TF_OK;
+}
+
 int tf_leaf_log2(int dtype, int64_t n) {
   if (dtype != TF_F32 && dtype != TF_F64) return -TF_EINVAL_DTYPE;
   return auto_leaf_log2(dtype, n);
@@ -594,7 +670,8 @@ int tf_workspace_size(int method, int dtype, int64_t rows, int64_t cols, int lea
   int lg;
   if ((rc = resolve_leaf(dtype, rows * cols, leaf_log2, &lg))) return rc;
   const int64_t P = (cols + (int64_t(1) << lg) - 1) >> lg;
-  if (partials_bytes) *partials_bytes = static_cast<size_t>(rows * P) * pair_bytes(method, dtype);
+  // sized for the largest leaf split (kMaxSplit unit pairs per leaf)
+  if (partials_bytes) *partials_bytes = static_cast<size_t>(rows * P * kMaxSplit) * pair_bytes(method, dtype);
   if (counters) *counters = rows;
   if (leaves) *leaves = P;
   return TF_OK;
@@ -618,15 +695,16 @@ int tf_reduce_rows(int method, int dtype, const void* x, const void* y, int64_t 
       return record_cuda_error();
     return TF_OK;
   }
-  size_t need = 0;
-  int64_t P = 0;
-  tf_workspace_size(method, dtype, rows, cols, lg, &need, nullptr, &P);
-  if (P > 1 && (!partials || partials_bytes < need || !counters || counters_len < rows))
+  int64_t P = (cols + (int64_t(1) << lg) - 1) >> lg;
+  const size_t min_need = static_cast<size_t>(rows * P) * pair_bytes(method, dtype);
+  if (P > 1 && (!partials || partials_bytes < min_need || !counters || counters_len < rows))
     return TF_EWORKSPACE;
+  const int64_t capacity = partials ? static_cast<int64_t>(partials_bytes / pair_bytes(method, dtype)) : 0;
   void* parts = partials;
   const bool dot = y != nullptr;
 #define TFB_CALL_LEAVES(M, T, DOT) \
-  launch_leaves<M, T, DOT>(x, y, ldx, ldy, rows, cols, lg, parts, counters, out_pairs, 1, s)
+  launch_leaves<M, T, DOT>(x, y, ldx, ldy, rows, cols, lg, parts, counters, out_pairs, 1, s, capacity, \
+                           counters ? counters_len : 0)
   TFB_DISPATCH(internal_method(method), dtype, dot, TFB_CALL_LEAVES);
 #undef TFB_CALL_LEAVES
 }

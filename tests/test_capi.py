@@ -64,8 +64,9 @@ def test_workspace_size(lib):
     from paper_1401_0248_b200 import Method, workspace_size
     import torch
     pb, cnt, leaves = workspace_size(Method.TWOFOLD_FAST, torch.float64, 1, 1 << 29)
-    assert leaves == (1 << 29) >> 16 and pb == leaves * 16 and cnt == 1
+    # partials are sized for the largest leaf split (4 unit pairs per leaf)
+    assert leaves == (1 << 29) >> 16 and pb == 4 * leaves * 16 and cnt == 1
     pb, cnt, leaves = workspace_size(Method.WIDE, torch.float32, 4096, 65536)
-    assert leaves == 1 and pb == 4096 * 16 and cnt == 4096  # wide pairs are binary64
+    assert leaves == 1 and pb == 4 * 4096 * 16 and cnt == 4096  # wide pairs are binary64
     pb, cnt, leaves = workspace_size(Method.KAHAN, torch.float32, 1, 1 << 24)
-    assert leaves == (1 << 24) >> 15 and pb == leaves * 8
+    assert leaves == (1 << 24) >> 15 and pb == 4 * leaves * 8

@@ -405,3 +405,30 @@ def test_cfg5_accuracy_at_full_scale_on_gpu(tfb, cuda):
     assert abs(Fraction(float(rr.value)) + Fraction(float(rr.error)) - S) <= 2 * n * eps * eps * A
     del x, y
     torch.cuda.empty_cache()
+
+
+def test_leaf_split_is_result_neutral(tfb, oracle, cuda):
+    """Splitting leaves over 1/2/4 CTAs (grid balance) never changes a bit."""
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    try:
+        for dt in (np.float32, np.float64):
+            for n in (5, 4097, 100_003, 1 << 20, (1 << 22) + 9):
+                xh = oracle.lcg_fill("mmix", n, 41, dt, True)
+                yh = oracle.lcg_fill("nr", n, 42, dt, True)
+                x, y = torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda)
+                for m in _methods(dt):
+                    meth = list(tfb.Method)[m]
+                    want = oracle.emulate(m, xh, yh)
+                    for split in (1, 2, 4):
+                        assert L.tf_set_leaf_split(split) == 0
+                        _same(tfb.reduce(meth, x, y).cpu().numpy(), want, (dt, n, m, split))
+                X = torch.from_numpy(oracle.lcg_fill("nr", 37 * 5000, 43, dt, True).reshape(37, 5000)).to(cuda)
+                ref = None
+                for split in (1, 2, 4):
+                    L.tf_set_leaf_split(split)
+                    got = tfb.reduce_rows(tfb.Method.TWOFOLD_RIGOROUS, X).cpu()
+                    ref = got if ref is None else ref
+                    assert torch.equal(got, ref)
+    finally:
+        L.tf_set_leaf_split(0)

@@ -78,7 +78,8 @@ def test_no_flush_to_zero_arithmetic(sass):
 
 
 def test_streaming_128bit_loads_in_vector_kernels(sass):
-    vec = [fn for fn in sass if "leaves_kernel" in fn and fn.endswith("ELb1EEEvPKT0_S3_llllilPNS_4PairINS_3AccIXT_ES1_E4typeEEEPjS9_i")]
+    # leaves_kernel<M, T, DOT, VEC=true, NT>
+    vec = [fn for fn in sass if re.search(r"leaves_kernelILi\dE[fd]Lb[01]ELb1ELi\d+E", fn)]
     assert vec
     for fn in vec:
         assert any(re.search(r"LDG\.E\.(NA\.)?\S*128", ln) for ln in sass[fn]), fn
