@@ -98,6 +98,14 @@ int tf_leaf_log2(int dtype, int64_t n);
  * value).  Result-neutral by construction: only the grid balance changes. */
 int tf_set_leaf_split(int split);
 
+/* Tuning knob (process-wide): loader of the grid reduction for 16-byte aligned
+ * inputs — 0 = automatic (default: TMA for dots streaming >= 512 MiB, else
+ * LDG), 1 = 128-bit streaming LDG, 2 = warp-specialised bulk-copy (TMA engine)
+ * pipeline, 4 stages x 16 KiB per operand, 3 = the same with 8 x 8 KiB.
+ * Results are bit-identical (same partition and trees); env TFB_LOADER sets
+ * the initial value. */
+int tf_set_loader(int loader);
+
 /* Scratch for rows x cols (1-D: rows = 1, cols = n) at leaf_log2 (0 = auto):
  *   partials: rows * leaves(cols) (value, error) pairs, any contents on entry;
  *   counters: `rows` uint32 retire-tickets, ZERO on entry and left zero on exit

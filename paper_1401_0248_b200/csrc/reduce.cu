@@ -96,7 +96,16 @@ template <int M> struct HasErr {
 // Balanced contiguous binary tree over the first `width` (power of two,
 // 1..256) threads' states; result valid in thread 0.  Level `off` merges
 // thread t (t % 2off == 0) with thread t + off as the right operand.
-template <int M, typename A>
+// CTA-level barrier for the first NT threads: __syncthreads when the whole CTA
+// takes part (BAR == 0), else named barrier BAR (warp-specialised kernels whose
+// producer warp must not join).
+template <int BAR, int NT>
+__device__ __forceinline__ void group_sync() {
+  if constexpr (BAR == 0) __syncthreads();
+  else asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+}
+
+template <int M, typename A, int BAR = 0, int NT = kThreads>
 __device__ __forceinline__ Pair<A> block_tree(Pair<A> st, Pair<A>* smem, int width) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -112,7 +121,7 @@ __device__ __forceinline__ Pair<A> block_tree(Pair<A> st, Pair<A>* smem, int wid
   }
   if (width > 32) {
     if (lane == 0) smem[warp] = st;
-    __syncthreads();
+    group_sync<BAR, NT>();
     if (warp == 0) {
       const int nw = width >> 5;
       st = lane < nw ? smem[lane] : zero_pair<A>();
@@ -126,7 +135,7 @@ __device__ __forceinline__ Pair<A> block_tree(Pair<A> st, Pair<A>* smem, int wid
         if ((lane & (2 * off - 1)) == 0) st = merge<M, A>(st, o);
       }
     }
-    __syncthreads();
+    group_sync<BAR, NT>();
   }
   return st;
 }
@@ -135,7 +144,7 @@ __device__ __forceinline__ Pair<A> block_tree(Pair<A> st, Pair<A>* smem, int wid
 // CTA.  If P2 >= 256, thread t first folds leaves [t*g, (t+1)*g), g = P2/256,
 // with a binary-counter stack (the same balanced shape, sequentially), then
 // the 256-thread tree finishes; otherwise threads < P2 hold one pair each.
-template <int M, typename A, int NT = kThreads>
+template <int M, typename A, int NT = kThreads, int BAR = 0>
 __device__ Pair<A> tree_over(const Pair<A>* parts, int64_t P, Pair<A>* smem) {
   int64_t P2 = 1;
   while (P2 < P) P2 <<= 1;
@@ -164,10 +173,10 @@ __device__ Pair<A> tree_over(const Pair<A>* parts, int64_t P, Pair<A>* smem) {
     }
     int lg = 0;
     while ((int64_t(1) << lg) < g) ++lg;
-    return block_tree<M, A>(stack[lg], smem, NT);
+    return block_tree<M, A, BAR, NT>(stack[lg], smem, NT);
   }
   Pair<A> cur = t < P ? ld_pair_cg(parts + t) : zero_pair<A>();
-  return block_tree<M, A>(cur, smem, static_cast<int>(P2));
+  return block_tree<M, A, BAR, NT>(cur, smem, static_cast<int>(P2));
 }
 
 template <typename T, bool DOT, int U>
@@ -417,6 +426,10 @@ __global__ void __launch_bounds__(kThreads) noread_kernel(const T* __restrict__ 
   out[blockIdx.x * int64_t(blockDim.x) + threadIdx.x] = st;
 }
 
+}  // namespace tfb
+#include "tma.cuh"
+namespace tfb {
+
 // ---------------------------------------------------------------------------
 // Host side.
 
@@ -493,6 +506,58 @@ static int choose_split(int64_t units, int fused) {
   return 1;
 }
 
+// Loader for aligned inputs: 0 = auto, 1 = 128-bit LDG streaming
+// (leaves_kernel), 2 = bulk-copy/TMA pipeline (leaves_tma_kernel, 4 stages x
+// 16 KiB per operand), 3 = TMA with 8 stages x 8 KiB.  Results are identical.
+// Auto (measured, profiles/r01_summary.md): TMA for dot products streaming
+// >= 512 MiB (cfg5 +1.1 %, cfg4 +2.5 %), LDG otherwise (sums and mid/small
+// sizes are faster with LDG's higher CTA occupancy).  Env TFB_LOADER or
+// tf_set_loader() override.
+static int g_loader = -1;
+static int loader_choice() {
+  if (g_loader < 0) {
+    const char* e = getenv("TFB_LOADER");
+    g_loader = e ? atoi(e) : 0;
+  }
+  return g_loader;
+}
+
+template <int M, typename T, bool DOT, int NS, int SR>
+static int launch_leaves_tma(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
+                             int leaf_log2, int64_t P, void* partials, void* counters, void* out,
+                             cudaStream_t stream) {
+  using A = typename Acc<M, T>::type;
+  auto kern = &leaves_tma_kernel<M, T, DOT, NS, SR>;
+  const size_t smem = TmaSmem<T, DOT, NS, SR>::kBytes;
+  static std::mutex mu;
+  static std::unordered_map<int, int> occ;  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int blocks = 0;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = occ.find(dev);
+    if (it == occ.end()) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+          cudaSuccess)
+        return record_cuda_error();
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, kTmaThreads, smem) != cudaSuccess ||
+          blocks < 1)
+        blocks = 1;
+      occ[dev] = blocks;
+    } else {
+      blocks = it->second;
+    }
+  }
+  const int64_t units = rows * P;
+  const int64_t slots = static_cast<int64_t>(device_sms()) * blocks;
+  const unsigned grid = static_cast<unsigned>(units < slots ? units : slots);
+  kern<<<grid, kTmaThreads, smem, stream>>>(px, py, ldx, ldy, rows, cols, leaf_log2, P,
+                                            static_cast<Pair<A>*>(partials), static_cast<unsigned*>(counters),
+                                            static_cast<Pair<A>*>(out));
+  return check_launch();
+}
+
 template <int M, typename T, bool DOT, bool VEC, int NT>
 static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                             int leaf_log2, int64_t P, void* partials, void* counters, void* out, int fused,
@@ -535,6 +600,17 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
                                                 counters, out, fused, stream))
   if (S == 4) return TFB_NT(64);
   if (S == 2) return TFB_NT(128);
+  int loader = loader_choice();
+  if (loader == 0) {
+    const int64_t bytes = rows * cols * static_cast<int64_t>(sizeof(T)) * (DOT ? 2 : 1);
+    loader = (DOT && bytes >= (int64_t(512) << 20)) ? 2 : 1;
+  }
+  if (vec && fused && loader == 2)
+    return launch_leaves_tma<M, T, DOT, 4, 4>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
+                                              out, stream);
+  if (vec && fused && loader == 3)
+    return launch_leaves_tma<M, T, DOT, 8, 2>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
+                                              out, stream);
   return TFB_NT(256);
 #undef TFB_NT
 }
@@ -650,6 +726,12 @@ static int resolve_leaf(int dtype, int64_t total, int leaf_log2, int* out) {
 using namespace tfb;
 
 extern "C" {
+
+int tf_set_loader(int loader) {
+  if (loader < 0 || loader > 3) return TF_EINVAL_ARG;
+  g_loader = loader;
+  return TF_OK;
+}
 
 int tf_set_leaf_split(int split) {
   if (split != 0 && split != 1 && split != 2 && split != 4) return TF_EINVAL_ARG;

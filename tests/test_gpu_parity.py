@@ -432,3 +432,32 @@ def test_leaf_split_is_result_neutral(tfb, oracle, cuda):
                     assert torch.equal(got, ref)
     finally:
         L.tf_set_leaf_split(0)
+
+
+def test_tma_loader_bit_identical(tfb, oracle, cuda):
+    """The bulk-copy (TMA engine) pipeline loader gives the same bits as the LDG loader
+    and the emulator: full and partial leaves, sums, dots, rows."""
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    try:
+        for dt in (np.float32, np.float64):
+            for n in (17, 4097, 100_003, (1 << 21) + 9):
+                xh = oracle.lcg_fill("mmix", n, 51, dt, True)
+                yh = oracle.lcg_fill("nr", n, 52, dt, True)
+                x, y = torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda)
+                for m in _methods(dt):
+                    meth = list(tfb.Method)[m]
+                    for yy, yyh in ((None, None), (y, yh)):
+                        want = oracle.emulate(m, xh, yyh)
+                        for loader in (1, 2):
+                            assert L.tf_set_loader(loader) == 0
+                            _same(tfb.reduce(meth, x, yy).cpu().numpy(), want, (dt, n, m, loader))
+            X = tfb.rows_scaled_normal(33, 70_000, seed=5, stream=0, dtype=torch.float32)
+            Y = tfb.rows_scaled_normal(33, 70_000, seed=5, stream=1, dtype=torch.float32)
+            L.tf_set_loader(0)
+            ref = tfb.reduce_rows(tfb.Method.TWOFOLD_FAST, X, Y).cpu()
+            for loader in (1, 2):
+                L.tf_set_loader(loader)
+                assert torch.equal(tfb.reduce_rows(tfb.Method.TWOFOLD_FAST, X, Y).cpu(), ref)
+    finally:
+        L.tf_set_loader(0)
