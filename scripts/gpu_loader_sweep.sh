@@ -1,7 +1,7 @@
 # LDG vs TMA-pipeline loaders (bit-identical) on every config; then the GPU tests.
 mkdir -p gpurun_out/loader
 timeout 600 python -m pytest tests -m gpu -q -x 2>&1 | tail -3
-for ld in 0 1 2; do
+for ld in 0 1 2 3; do
   for c in cfg1 cfg2-small cfg2 cfg2-dott cfg3 cfg3-sumk cfg4 cfg5; do
     TFB_LOADER=$ld timeout 300 python bench.py --config $c --steps 30 --warmup 3 --no-cpu --no-e2e > gpurun_out/loader/$c.$ld.json 2> gpurun_out/loader/$c.$ld.err
   done
