@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--leaf-log2", type=int, default=0, help="override the auto leaf size (sweeps)")
     ap.add_argument("--graph", action="store_true", help="replay the timed steps from a CUDA graph")
+    ap.add_argument("--force-collective", action="store_true",
+                    help="init NCCL and run the all-gather + merge path even at world size 1 (plumbing check)")
     return ap.parse_args()
 
 
@@ -232,7 +234,7 @@ def run_reference(args):
                          "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -248,8 +250,11 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    if world > 1 or args.force_collective:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    use_dist = dist.is_initialized()
 
     cfg_key, method_name, n_rank, flush = WORKLOADS[args.config]
     cfg = CONFIGS[cfg_key]
@@ -283,7 +288,8 @@ def run_ours(args):
         xi, yi = copies[i % R]
         if rows:
             return tfb.reduce_rows(method, xi, yi, leaf_log2=args.leaf_log2)
-        return tfb.sharded_reduce(method, xi, yi, n_global=n_global if n_rank else n, leaf_log2=leaf_arg)
+        return tfb.sharded_reduce(method, xi, yi, n_global=n_global if n_rank else n, leaf_log2=leaf_arg,
+                                  force_collective=args.force_collective)
 
     def kernel_launch(i):
         xi, yi = copies[i % R]
@@ -328,30 +334,32 @@ def run_ours(args):
         return e0.elapsed_time(e1)
 
     # --- device-timed steps -------------------------------------------------
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     with clocks:
         elapsed_ms = timed(step)
     torch.cuda.synchronize()
-    if world > 1:
+    if use_dist:
         dist.barrier()
     t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms = t.item() / K_eff
     value = n * world * K_eff / (t.item() * 1e-3) / 1e9
-    launches_per_step = 1 + (1 if world > 1 and not rows else 0)
+    launches_per_step = 1 + (1 if (world > 1 or args.force_collective) and not rows else 0)
 
     # --- kernel-only timing (roofline of the reduction kernel) ---------------
     kernel_ms = timed(kernel_launch) / K_eff
+    kernel_launch(0)
+    from paper_1401_0248_b200 import _lib as _tl
+    launch_desc = _tl.lib().tf_last_launch().decode()
     peak, peak_src = measured_peak()
     achieved = bytes_per_step / (kernel_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic_for(args.config), "peak_source": peak_src,
-                "kernel": f"leaves_kernel<{method_name},{'f64' if item == 8 else 'f32'},"
-                          f"{'dot' if y is not None else 'sum'}> (fused leaf + tree)",
+                "kernel": launch_desc + " (fused leaf + tree, one launch per step)",
                 "algorithmic_bytes_per_launch": bytes_per_step, "kernel_ms": kernel_ms,
                 "kernel_share_of_step": kernel_ms / step_ms if step_ms else None,
                 "timing": ("CUDA graph of K launches, events around one replay" if use_graph
@@ -376,12 +384,13 @@ def run_ours(args):
                 return r.values.cpu()
             return tfb.sharded_run(method, xh, yh, n_global=n_global if n_rank else n, leaf_log2=lg)
 
+
         r0 = e2e_step()  # warm-up (also allocates the staging buffers)
         if not rows:
             assert float(r0.value) == float(res_dev[0]) and (
                 method not in (tfb.Method.TWOFOLD_FAST, tfb.Method.TWOFOLD_RIGOROUS)
                 or float(r0.error) == float(res_dev[1])), "e2e result differs from the device path"
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
         w0 = time.perf_counter()
@@ -389,7 +398,7 @@ def run_ours(args):
             e2e_step()
         torch.cuda.synchronize()
         wall = time.perf_counter() - w0
-        if world > 1:
+        if use_dist:
             tw = torch.tensor([wall], dtype=torch.float64, device=dev)
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)
             wall = tw.item()
@@ -436,15 +445,35 @@ def run_ours(args):
                    "error": float(res_dev[1]) if not rows else None},
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
+        emit(line)
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     return 0
 
 
+def _reserve_stdout():
+    """The contract is ONE JSON line on stdout: native libraries (NCCL's version
+    banner, driver warnings) write to fd 1, so fd 1 is pointed at stderr for the
+    run and the JSON line goes to a saved copy of the real stdout."""
+    global _OUT
+    real = os.dup(1)
+    os.dup2(2, 1)
+    _OUT = os.fdopen(real, "w")
+
+
+_OUT = None
+
+
+def emit(line: dict) -> None:
+    out = _OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
     args = parse()
+    _reserve_stdout()
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -98,6 +98,10 @@ int tf_leaf_log2(int dtype, int64_t n);
  * value).  Result-neutral by construction: only the grid balance changes. */
 int tf_set_leaf_split(int split);
 
+/* Human-readable description of the calling thread's last grid-reduction
+ * launch (kernel, template arguments, grid, block, units, leaf size). */
+const char* tf_last_launch(void);
+
 /* Tuning knob (process-wide): loader of the grid reduction for 16-byte aligned
  * inputs — 0 = automatic (default: TMA for dots streaming >= 512 MiB, else
  * LDG), 1 = 128-bit streaming LDG, 2 = warp-specialised bulk-copy (TMA engine)

@@ -490,7 +490,15 @@ int auto_leaf_log2(int dtype, int64_t total) {
 // counts).  Result-neutral (see leaves_kernel); TFB_SPLIT=1|2|4 or
 // tf_set_leaf_split() override it.
 constexpr int kMaxSplit = 4;
-static int g_split_override = -1;  // -1: read TFB_SPLIT once; 0: auto; 1|2|4: forced
+static int g_split_override = -1;
+
+// Description of the calling thread's last grid-reduction launch (tf_last_launch).
+static thread_local char g_last_launch[192] = {0};
+static const char* method_tag(int M) {
+  static const char* tags[] = {"direct", "wide", "twofold-fast", "twofold-rigorous", "kahan",
+                               "twofold-fast+TP", "twofold-rigorous+TP"};
+  return M >= 0 && M < 7 ? tags[M] : "?";
+}  // -1: read TFB_SPLIT once; 0: auto; 1|2|4: forced
 
 static int choose_split(int64_t units, int fused) {
   if (!fused) return 1;  // leaves-only mode promises one pair per leaf
@@ -552,6 +560,10 @@ static int launch_leaves_tma(const T* px, const T* py, int64_t ldx, int64_t ldy,
   const int64_t units = rows * P;
   const int64_t slots = static_cast<int64_t>(device_sms()) * blocks;
   const unsigned grid = static_cast<unsigned>(units < slots ? units : slots);
+  snprintf(g_last_launch, sizeof(g_last_launch),
+           "leaves_tma_kernel<%s,%s,%s,NS=%d,SR=%d> grid=%u block=%d smem=%zu units=%lld leaf_log2=%d",
+           method_tag(M), sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", NS, SR, grid, kTmaThreads, smem,
+           static_cast<long long>(units), leaf_log2);
   kern<<<grid, kTmaThreads, smem, stream>>>(px, py, ldx, ldy, rows, cols, leaf_log2, P,
                                             static_cast<Pair<A>*>(partials), static_cast<unsigned*>(counters),
                                             static_cast<Pair<A>*>(out));
@@ -568,6 +580,10 @@ static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, 
   const int64_t slots = static_cast<int64_t>(device_sms()) * occupancy_of(fn, NT);
   const int64_t grid64 = units < slots ? units : slots;
   const unsigned grid = static_cast<unsigned>(grid64 > 0 ? grid64 : 1);
+  snprintf(g_last_launch, sizeof(g_last_launch),
+           "leaves_kernel<%s,%s,%s,%s,NT=%d> grid=%u block=%d units=%lld leaf_log2=%d", method_tag(M),
+           sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", VEC ? "ldg128" : "scalar", NT, grid, NT,
+           static_cast<long long>(units), leaf_log2);
   leaves_kernel<M, T, DOT, VEC, NT><<<grid, NT, 0, stream>>>(
       px, py, ldx, ldy, rows, cols, leaf_log2, P, static_cast<Pair<A>*>(partials),
       static_cast<unsigned*>(counters), static_cast<Pair<A>*>(out), fused);
@@ -726,6 +742,8 @@ static int resolve_leaf(int dtype, int64_t total, int leaf_log2, int* out) {
 using namespace tfb;
 
 extern "C" {
+
+const char* tf_last_launch(void) { return g_last_launch; }
 
 int tf_set_loader(int loader) {
   if (loader < 0 || loader > 3) return TF_EINVAL_ARG;

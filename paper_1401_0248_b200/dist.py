@@ -63,7 +63,7 @@ def _world(group) -> tuple[int, int]:
 def sharded_reduce(method: Method, x_local: torch.Tensor, y_local: torch.Tensor | None = None, *,
                    n_global: int, leaf_log2: int = 0, group=None,
                    local_reduce: LocalReduce | None = None, merge: Merge | None = None,
-                   track_product: bool = False) -> torch.Tensor:
+                   track_product: bool = False, force_collective: bool = False) -> torch.Tensor:
     """Raw (value, error) pair of the global array, identical on every rank.
 
     x_local / y_local: this rank's shard (CUDA tensors for the default
@@ -76,8 +76,8 @@ def sharded_reduce(method: Method, x_local: torch.Tensor, y_local: torch.Tensor 
     else:
         local = local_reduce(method, x_local, y_local, lg)
     _, world = _world(group)
-    if world == 1:
-        return local
+    if world == 1 and not (force_collective and dist.is_available() and dist.is_initialized()):
+        return local  # force_collective exercises the all-gather + merge path at world size 1
     parts = [torch.empty_like(local) for _ in range(world)]
     dist.all_gather(parts, local.contiguous(), group=group)
     gathered = torch.stack(parts, 0)
