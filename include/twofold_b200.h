@@ -185,6 +185,12 @@ int tf_fill(int dist, int dtype, uint64_t seed, uint64_t stream_id, uint64_t off
             int64_t n, double p0, double p1, double p2, int64_t total,
             void* out, void* stream);
 
+/* Host twin of tf_fill for the integer-exact distributions (UNIFORM01,
+ * UNIFORM_SYM, ILLCOND): fills a HOST buffer bit-identically to the device
+ * stream (SURVEY.md §8(b) tf_philox_fill_host).  nthreads <= 0: all cores. */
+int tf_fill_host(int dist, int dtype, uint64_t seed, uint64_t stream_id, uint64_t offset, int64_t n,
+                 double p0, double p1, double p2, int64_t total, void* out, int nthreads);
+
 /* The reference's LCG generators (lcg.py:75-116), bit-identical to
  * twofold.fill(kind, offset+n, seed, dtype, sym)[offset:]: kind 0 = Numerical
  * Recipes (32-bit), 1 = MMIX (64-bit); state jump-ahead makes any slice

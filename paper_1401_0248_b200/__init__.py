@@ -40,7 +40,7 @@ from .api import (
 )
 from .dist import shard_range, sharded_reduce, sharded_run
 from .exact import ExactValue, exact_dot, exact_sum, relative_error
-from .gen import CONFIGS, lcg_fill, make_inputs, philox_fill, rows_scaled_normal
+from .gen import CONFIGS, lcg_fill, make_inputs, philox_fill, philox_fill_host, rows_scaled_normal
 
 __version__ = "0.1.0"
 
@@ -52,6 +52,6 @@ __all__ = [
     "reduce", "reduce_rows", "sum_rows", "dot_rows", "merge_pairs", "workspace_size", "leaf_log2_for",
     "shard_range", "sharded_reduce", "sharded_run",
     "ExactValue", "exact_sum", "exact_dot", "relative_error",
-    "philox_fill", "lcg_fill", "rows_scaled_normal", "make_inputs", "CONFIGS",
+    "philox_fill", "philox_fill_host", "lcg_fill", "rows_scaled_normal", "make_inputs", "CONFIGS",
     "__version__",
 ]

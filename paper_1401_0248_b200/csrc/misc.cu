@@ -6,6 +6,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstring>
+#include <thread>
+#include <vector>
 
 #include "eft.cuh"
 #include "philox.cuh"
@@ -318,6 +320,65 @@ int tf_lcg_fill(int kind, int dtype, uint64_t seed, int sym, int64_t offset, int
     lcg_fill_kernel<double><<<g, 256, 0, s>>>(kind, seed, sym, static_cast<uint64_t>(offset), n,
                                               static_cast<double*>(out));
   return check_launch();
+}
+
+// Host twin of tf_fill for the integer-exact distributions (uniform01,
+// uniform_sym, illcond): the same philox.cuh code compiled for the CPU, so a
+// host buffer can be filled bit-identically to the device stream (e.g. the
+// input of an end-to-end call).  nthreads <= 0: all hardware threads.
+int tf_fill_host(int dist, int dtype, uint64_t seed, uint64_t stream_id, uint64_t offset, int64_t n,
+                 double p0, double p1, double p2, int64_t total, void* out, int nthreads) {
+  if (dist != TF_DIST_UNIFORM01 && dist != TF_DIST_UNIFORM_SYM && dist != TF_DIST_ILLCOND) return TF_EINVAL_ARG;
+  if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
+  if (n < 0) return TF_EINVAL_SHAPE;
+  if (n == 0) return TF_OK;
+  if (!out) return TF_EINVAL_ARG;
+  if (dist == TF_DIST_ILLCOND &&
+      (total <= 0 || offset + static_cast<uint64_t>(n) > static_cast<uint64_t>(total)))
+    return TF_EINVAL_SHAPE;
+  auto work = [=](int64_t lo, int64_t hi) {
+    for (int64_t i = lo; i < hi; ++i) {
+      const uint64_t p = offset + static_cast<uint64_t>(i);
+      double d;
+      float f = 0.0f;
+      if (dist == TF_DIST_ILLCOND) {
+        const uint64_t tot = static_cast<uint64_t>(total);
+        const uint64_t q = feistel_permute(p, tot, seed);
+        const uint64_t h = tot / 4;
+        if (q < 2 * h) {
+          const uint64_t k = q < h ? q : q - h;
+          const volatile double prod = p1 * u01_f64(philox_at(seed, stream_id, k));  // no contraction
+          const double b = p0 + prod;
+          d = q < h ? b : -b;
+        } else {
+          d = p2 * u01_f64(philox_at(seed, stream_id + 1, q));
+        }
+        f = static_cast<float>(d);
+      } else if (dtype == TF_F32) {
+        f = u01_f32(philox_at(seed, stream_id, p));
+        if (dist == TF_DIST_UNIFORM_SYM) f = 2.0f * f - 1.0f;  // exact
+        d = f;
+      } else {
+        d = u01_f64(philox_at(seed, stream_id, p));
+        if (dist == TF_DIST_UNIFORM_SYM) d = 2.0 * d - 1.0;    // exact
+      }
+      if (dtype == TF_F32) static_cast<float*>(out)[i] = f;
+      else static_cast<double*>(out)[i] = d;
+    }
+  };
+  int nt = nthreads > 0 ? nthreads : static_cast<int>(std::thread::hardware_concurrency());
+  if (nt < 1) nt = 1;
+  if (nt > 256) nt = 256;
+  if (n < (int64_t(1) << 16)) nt = 1;
+  std::vector<std::thread> pool;
+  int64_t base = 0;
+  for (int t = 0; t < nt; ++t) {
+    const int64_t len = n / nt + (t < n % nt ? 1 : 0);
+    pool.emplace_back(work, base, base + len);
+    base += len;
+  }
+  for (auto& th : pool) th.join();
+  return TF_OK;
 }
 
 int tf_fill_rows_scaled(int dtype, uint64_t seed, uint64_t stream_id, uint64_t scale_stream,

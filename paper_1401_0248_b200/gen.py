@@ -45,6 +45,21 @@ def philox_fill(dist: str, n: int, *, seed: int, stream: int = 0, offset: int = 
     return out
 
 
+def philox_fill_host(dist: str, n: int, *, seed: int, stream: int = 0, offset: int = 0,
+                     dtype: torch.dtype = torch.float64, params=(1e8, 9e8, 1e-3), total: int | None = None,
+                     pin_memory: bool = False, nthreads: int = 0) -> torch.Tensor:
+    """Host (CPU) twin of philox_fill for the integer-exact distributions:
+    bit-identical bytes in a host tensor (optionally pinned, for e2e inputs)."""
+    if dist not in ("uniform01", "uniform_sym", "illcond"):
+        raise ValueError("the host twin covers uniform01, uniform_sym and illcond")
+    out = torch.empty(n, dtype=dtype, pin_memory=pin_memory)
+    code = _lib.TF_F32 if dtype == torch.float32 else _lib.TF_F64
+    tot = total if total is not None else offset + n
+    check(lib().tf_fill_host(_DIST[dist], code, seed, stream, offset, n, params[0], params[1], params[2], tot,
+                             out.data_ptr(), nthreads), "tf_fill_host")
+    return out
+
+
 def lcg_fill(kind: str, n: int, seed: int = 1, dtype: torch.dtype = torch.float64, sym: bool = False, *,
              offset: int = 0, device=None, out: torch.Tensor | None = None) -> torch.Tensor:
     """The reference's LCG data on the device, bit-identical to

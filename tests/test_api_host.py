@@ -92,3 +92,18 @@ def test_leaf_rule_and_shard_ranges(oracle):
     assert spans[0][0] == 0 and spans[-1][1] == n and all(a % 4096 == 0 for a, _ in spans)
     with pytest.raises(ValueError):
         tfb.shard_range(10, 3, 3, 9)
+
+
+def test_product_host_twin_matches_oracle_twin(oracle):
+    """tf_fill_host (product, CPU) == the oracle's independent Philox restatement
+    (and, in test_gpu_parity.py, == the device stream)."""
+    for dist in ("uniform01", "uniform_sym"):
+        for dt, ndt in ((torch.float32, np.float32), (torch.float64, np.float64)):
+            a = tfb.philox_fill_host(dist, 100_003, seed=9, stream=3, offset=77, dtype=dt).numpy()
+            b = oracle.philox_fill(dist, 100_003, 9, 3, 77, ndt)
+            assert a.tobytes() == b.tobytes(), (dist, dt)
+    a = tfb.philox_fill_host("illcond", 1 << 16, seed=2, total=1 << 16).numpy()
+    b = oracle.philox_fill("illcond", 1 << 16, 2, 0, 0, np.float64, total=1 << 16)
+    assert a.tobytes() == b.tobytes()
+    with pytest.raises(ValueError):
+        tfb.philox_fill_host("normal", 10, seed=1)
