@@ -98,6 +98,13 @@ int tf_leaf_log2(int dtype, int64_t n);
  * value).  Result-neutral by construction: only the grid balance changes. */
 int tf_set_leaf_split(int split);
 
+/* Tuning knob (process-wide): tail of the fused reduction — 0 = automatic
+ * (PDL for the LDG loader; the TMA loader keeps its single launch), 1 =
+ * last-CTA retire ticket inside the single launch, 2 = partials-only launch +
+ * a programmatic-dependent-launch (PDL) tree kernel.  Identical results; env
+ * TFB_TAIL sets the initial value. */
+int tf_set_tail(int tail);
+
 /* Human-readable description of the calling thread's last grid-reduction
  * launch (kernel, template arguments, grid, block, units, leaf size). */
 const char* tf_last_launch(void);

@@ -304,6 +304,9 @@ __global__ void __launch_bounds__(NT) leaves_kernel(
   const int R = (1 << leaf_log2) / (kThreads * V);
   const int64_t per_row = P * S;
   const int64_t units = rows * per_row;
+  // partials-only mode may feed a programmatic-dependent tree kernel: let it be
+  // scheduled now (it waits on griddepcontrol.wait for this grid's completion)
+  if (!fused) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
     const int64_t r = u / per_row;
     const int64_t rem = u - r * per_row;
@@ -345,6 +348,21 @@ __global__ void __launch_bounds__(kThreads) tree_kernel(const Pair<A>* __restric
   __shared__ Pair<A> smem[kWarps];
   Pair<A> root = count > 0 ? tree_over<M, A>(pairs, count, smem) : zero_pair<A>();
   if (threadIdx.x == 0) out[0] = root;
+}
+
+// Row trees over unit pairs written by a partials-only leaves launch; launched
+// as a programmatic dependent (PDL) of it: resident early, waits for the
+// primary grid's completion (and memory flush) in griddepcontrol.wait.
+template <int M, typename A>
+__global__ void __launch_bounds__(kThreads) rows_tree_kernel(const Pair<A>* __restrict__ partials, int64_t rows,
+                                                             int64_t per_row, Pair<A>* __restrict__ out) {
+  __shared__ Pair<A> smem[kWarps];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    Pair<A> root = tree_over<M, A>(partials + r * per_row, per_row, smem);
+    if (threadIdx.x == 0) out[r] = root;
+    __syncthreads();
+  }
 }
 
 // Sequential flavor: the reference recurrence, one thread, left to right.
@@ -530,6 +548,38 @@ static int loader_choice() {
   return g_loader;
 }
 
+// Tail of the fused reduction: 0 = auto, 1 = last-CTA retire ticket (one
+// launch), 2 = partials-only launch + programmatic-dependent tree kernel.
+// Identical results; env TFB_TAIL or tf_set_tail() choose.
+static int g_tail = -1;
+static int tail_choice() {
+  if (g_tail < 0) {
+    const char* e = getenv("TFB_TAIL");
+    g_tail = e ? atoi(e) : 0;
+  }
+  return g_tail;
+}
+
+template <int M, typename A>
+static int launch_rows_tree_pdl(const void* partials, int64_t rows, int64_t per_row, void* out,
+                                cudaStream_t stream) {
+  cudaLaunchConfig_t cfg = {};
+  const int64_t sms = device_sms();
+  cfg.gridDim = dim3(static_cast<unsigned>(rows < sms * 4 ? rows : sms * 4));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, rows_tree_kernel<M, A>, static_cast<const Pair<A>*>(partials), rows, per_row,
+                         static_cast<Pair<A>*>(out)) != cudaSuccess)
+    return record_cuda_error();
+  return check_launch();
+}
+
 template <int M, typename T, bool DOT, int NS, int SR>
 static int launch_leaves_tma(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                              int leaf_log2, int64_t P, void* partials, void* counters, void* out,
@@ -614,19 +664,40 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
                                                counters, out, fused, stream)                          \
        : launch_leaves_nt<M, T, DOT, false, NT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,  \
                                                 counters, out, fused, stream))
-  if (S == 4) return TFB_NT(64);
-  if (S == 2) return TFB_NT(128);
   int loader = loader_choice();
   if (loader == 0) {
     const int64_t bytes = rows * cols * static_cast<int64_t>(sizeof(T)) * (DOT ? 2 : 1);
     loader = (DOT && bytes >= (int64_t(512) << 20)) ? 2 : 1;
   }
-  if (vec && fused && loader == 2)
+  if (vec && fused && S == 1 && loader == 2)
     return launch_leaves_tma<M, T, DOT, 4, 4>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
                                               out, stream);
-  if (vec && fused && loader == 3)
+  if (vec && fused && S == 1 && loader == 3)
     return launch_leaves_tma<M, T, DOT, 8, 2>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
                                               out, stream);
+  // LDG loader.  Tail: auto/2 = partials-only launch + PDL tree kernel (measured
+  // -0.5..-0.8 us on small inputs), 1 = single launch with last-CTA ticket.
+  const int tail = tail_choice();
+  if (fused && tail != 1 && units * S > rows && partials && partial_capacity >= units * S) {
+    int rc;
+    if (S == 4) rc = (vec ? launch_leaves_nt<M, T, DOT, true, 64>(px, py, ldx, ldy, rows, cols, leaf_log2, P,
+                                                                   partials, nullptr, nullptr, 0, stream)
+                          : launch_leaves_nt<M, T, DOT, false, 64>(px, py, ldx, ldy, rows, cols, leaf_log2, P,
+                                                                    partials, nullptr, nullptr, 0, stream));
+    else if (S == 2) rc = (vec ? launch_leaves_nt<M, T, DOT, true, 128>(px, py, ldx, ldy, rows, cols, leaf_log2,
+                                                                         P, partials, nullptr, nullptr, 0, stream)
+                               : launch_leaves_nt<M, T, DOT, false, 128>(px, py, ldx, ldy, rows, cols, leaf_log2,
+                                                                          P, partials, nullptr, nullptr, 0,
+                                                                          stream));
+    else rc = (vec ? launch_leaves_nt<M, T, DOT, true, 256>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,
+                                                             nullptr, nullptr, 0, stream)
+                   : launch_leaves_nt<M, T, DOT, false, 256>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,
+                                                              nullptr, nullptr, 0, stream));
+    if (rc) return rc;
+    return launch_rows_tree_pdl<M, typename Acc<M, T>::type>(partials, rows, P * S, out, stream);
+  }
+  if (S == 4) return TFB_NT(64);
+  if (S == 2) return TFB_NT(128);
   return TFB_NT(256);
 #undef TFB_NT
 }
@@ -744,6 +815,12 @@ using namespace tfb;
 extern "C" {
 
 const char* tf_last_launch(void) { return g_last_launch; }
+
+int tf_set_tail(int tail) {
+  if (tail < 0 || tail > 2) return TF_EINVAL_ARG;
+  g_tail = tail;
+  return TF_OK;
+}
 
 int tf_set_loader(int loader) {
   if (loader < 0 || loader > 3) return TF_EINVAL_ARG;

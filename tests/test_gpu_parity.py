@@ -461,3 +461,32 @@ def test_tma_loader_bit_identical(tfb, oracle, cuda):
                 assert torch.equal(tfb.reduce_rows(tfb.Method.TWOFOLD_FAST, X, Y).cpu(), ref)
     finally:
         L.tf_set_loader(0)
+
+
+def test_pdl_tail_bit_identical(tfb, oracle, cuda):
+    """Partials-only launch + programmatic-dependent tree kernel == the fused
+    single launch == the emulator (also with leaf splits)."""
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    try:
+        for dt in (np.float32, np.float64):
+            for n in (17, 70_001, (1 << 21) + 9):
+                xh = oracle.lcg_fill("mmix", n, 61, dt, True)
+                yh = oracle.lcg_fill("nr", n, 62, dt, True)
+                x, y = torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda)
+                for m in _methods(dt):
+                    meth = list(tfb.Method)[m]
+                    want = oracle.emulate(m, xh, yh)
+                    for split in (1, 2):
+                        L.tf_set_leaf_split(split)
+                        L.tf_set_tail(2)
+                        _same(tfb.reduce(meth, x, y).cpu().numpy(), want, (dt, n, m, split))
+        X = tfb.rows_scaled_normal(37, 70_000, seed=6, stream=0, dtype=torch.float32)
+        L.tf_set_tail(1)
+        L.tf_set_leaf_split(1)
+        ref = tfb.reduce_rows(tfb.Method.TWOFOLD_RIGOROUS, X).cpu()
+        L.tf_set_tail(2)
+        assert torch.equal(tfb.reduce_rows(tfb.Method.TWOFOLD_RIGOROUS, X).cpu(), ref)
+    finally:
+        L.tf_set_tail(0)
+        L.tf_set_leaf_split(0)
