@@ -88,7 +88,6 @@ def cpu_model() -> str:
 
 
 def workload_desc(name, cfg, method, n_rank, world):
-    from paper_1401_0248_b200.gen import CONFIGS  # noqa: F401
     d = {
         "workload": (f"{name}: {cfg.note}; {method} on {n_rank} elements per rank"
                      + (f" (rank r owns [r*2^29,(r+1)*2^29) of the 2^32 stream; N=8 is cfg5 in full)"

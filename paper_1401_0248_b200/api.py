@@ -23,6 +23,7 @@ fallback: without the CUDA library or a GPU every compute call raises.
 
 from __future__ import annotations
 
+import ctypes
 import threading
 from dataclasses import dataclass
 from enum import Enum
@@ -262,22 +263,12 @@ _scratch = _Scratch()
 
 
 def workspace_size(method: Method, dtype: torch.dtype, rows: int, cols: int, leaf_log2: int = 0):
-    pb = _c_size()
-    cnt = _c_i64()
-    leaves = _c_i64()
+    pb = ctypes.c_size_t(0)
+    cnt = ctypes.c_int64(0)
+    leaves = ctypes.c_int64(0)
     check(lib().tf_workspace_size(_METHOD_ID[method], _dtype_code(dtype), rows, cols, leaf_log2,
                                   pb, cnt, leaves), "tf_workspace_size")
     return pb.value, cnt.value, leaves.value
-
-
-def _c_size():
-    import ctypes
-    return ctypes.c_size_t(0)
-
-
-def _c_i64():
-    import ctypes
-    return ctypes.c_int64(0)
 
 
 def leaf_log2_for(dtype: torch.dtype, n: int) -> int:

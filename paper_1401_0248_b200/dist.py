@@ -24,7 +24,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .api import Method, SumResult, Twofold, _TWOFOLD_METHODS, _np_type, leaf_log2_for, merge_pairs, reduce
+from .api import Method, SumResult, Twofold, _TWOFOLD_METHODS, _np_type, leaf_log2_for, merge_pairs
 
 LocalReduce = Callable[[Method, torch.Tensor, "torch.Tensor | None", int], torch.Tensor]
 Merge = Callable[[Method, torch.Tensor], torch.Tensor]
@@ -101,4 +101,4 @@ def sharded_run(method: Method, x_local, y_local=None, *, n_global: int, leaf_lo
     return SumResult(Twofold(t(v), t(0)), n_global)
 
 
-__all__ = ["shard_range", "sharded_reduce", "sharded_run", "reduce"]
+__all__ = ["shard_range", "sharded_reduce", "sharded_run"]

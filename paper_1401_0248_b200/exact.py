@@ -15,7 +15,6 @@ import threading
 from dataclasses import dataclass
 from fractions import Fraction
 
-import numpy as np
 import torch
 
 from . import _lib
