@@ -17,6 +17,19 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Debug builds (-DTFB_DEBUG=1, scripts/build_debug.sh) assert every global
+// access range and scratch capacity on the device (compute-sanitizer is not
+// available on the GPU pool; this is the substitute).
+#ifndef TFB_DEBUG
+#define TFB_DEBUG 0
+#endif
+#if TFB_DEBUG
+#include <cassert>
+#define TFB_CHECK(cond) assert(cond)
+#else
+#define TFB_CHECK(cond) ((void)0)
+#endif
+
 namespace tfb {
 
 enum Method : int {

@@ -51,6 +51,7 @@ __device__ __forceinline__ void deposit(long long* acc, double v) {
     s = ebits - 1;  // normal: m * 2^(ebits - 1075) = m * 2^(ebits-1 - 1074)
   }
   const int d = s >> 5, r = s & 31;
+  TFB_CHECK(d >= 0 && d + 2 < kLimbs);
   const unsigned long long lo = m << r;                       // bits 0..63 of m << r
   const unsigned long long hi = r ? (m >> (64 - r)) : 0ull;    // bits 64..84
   long long c0 = static_cast<long long>(lo & 0xFFFFFFFFull);

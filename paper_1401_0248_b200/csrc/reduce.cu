@@ -214,7 +214,9 @@ __device__ __forceinline__ Pair<typename Acc<M, T>::type> leaf_chain(
   constexpr int V = Vec<T>::V;
   Pair<A> st = zero_pair<A>();
   const int64_t L = static_cast<int64_t>(R) * kThreads * V;
+  TFB_CHECK(t >= 0 && t < kThreads && start >= 0);
   if (VEC && start + L <= n) {
+    TFB_CHECK((reinterpret_cast<uintptr_t>(x + start) & 15u) == 0);
     const VT* xv = reinterpret_cast<const VT*>(x + start) + t;
     const VT* yv = DOT ? reinterpret_cast<const VT*>(y + start) + t : nullptr;
     // Software pipeline: batch k+U is in flight while batch k is consumed, so
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(NT) leaves_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy,
     int64_t rows, int64_t cols, int leaf_log2, int64_t P,
     Pair<typename Acc<M, T>::type>* __restrict__ partials, unsigned* __restrict__ counters,
-    Pair<typename Acc<M, T>::type>* __restrict__ out, int fused) {
+    Pair<typename Acc<M, T>::type>* __restrict__ out, int fused, int64_t part_cap) {
   using A = typename Acc<M, T>::type;
   constexpr int V = Vec<T>::V;
   constexpr int S = kThreads / NT;
@@ -318,6 +320,7 @@ __global__ void __launch_bounds__(NT) leaves_kernel(
         xr, yr, l << leaf_log2, cols, R, part * NT + static_cast<int>(threadIdx.x));
     st = block_tree<M, A>(st, smem, NT);
     if (!fused) {
+      TFB_CHECK(u < part_cap);
       if (threadIdx.x == 0) partials[u] = st;
       continue;
     }
@@ -326,6 +329,7 @@ __global__ void __launch_bounds__(NT) leaves_kernel(
       continue;
     }
     if (threadIdx.x == 0) {
+      TFB_CHECK(u < part_cap && counters != nullptr);
       partials[u] = st;
       s_last = (retire_ticket(&counters[r]) == static_cast<unsigned>(per_row - 1));
     }
@@ -355,9 +359,11 @@ __global__ void __launch_bounds__(kThreads) tree_kernel(const Pair<A>* __restric
 // primary grid's completion (and memory flush) in griddepcontrol.wait.
 template <int M, typename A>
 __global__ void __launch_bounds__(kThreads) rows_tree_kernel(const Pair<A>* __restrict__ partials, int64_t rows,
-                                                             int64_t per_row, Pair<A>* __restrict__ out) {
+                                                             int64_t per_row, Pair<A>* __restrict__ out,
+                                                             int64_t part_cap) {
   __shared__ Pair<A> smem[kWarps];
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  TFB_CHECK(rows * per_row <= part_cap);
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     Pair<A> root = tree_over<M, A>(partials + r * per_row, per_row, smem);
     if (threadIdx.x == 0) out[r] = root;
@@ -562,7 +568,7 @@ static int tail_choice() {
 
 template <int M, typename A>
 static int launch_rows_tree_pdl(const void* partials, int64_t rows, int64_t per_row, void* out,
-                                cudaStream_t stream) {
+                                cudaStream_t stream, int64_t part_cap) {
   cudaLaunchConfig_t cfg = {};
   const int64_t sms = device_sms();
   cfg.gridDim = dim3(static_cast<unsigned>(rows < sms * 4 ? rows : sms * 4));
@@ -575,7 +581,7 @@ static int launch_rows_tree_pdl(const void* partials, int64_t rows, int64_t per_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (cudaLaunchKernelEx(&cfg, rows_tree_kernel<M, A>, static_cast<const Pair<A>*>(partials), rows, per_row,
-                         static_cast<Pair<A>*>(out)) != cudaSuccess)
+                         static_cast<Pair<A>*>(out), part_cap) != cudaSuccess)
     return record_cuda_error();
   return check_launch();
 }
@@ -623,7 +629,7 @@ static int launch_leaves_tma(const T* px, const T* py, int64_t ldx, int64_t ldy,
 template <int M, typename T, bool DOT, bool VEC, int NT>
 static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                             int leaf_log2, int64_t P, void* partials, void* counters, void* out, int fused,
-                            cudaStream_t stream) {
+                            cudaStream_t stream, int64_t part_cap = INT64_MAX) {
   using A = typename Acc<M, T>::type;
   const void* fn = reinterpret_cast<const void*>(&leaves_kernel<M, T, DOT, VEC, NT>);
   const int64_t units = rows * P * (kThreads / NT);
@@ -636,7 +642,7 @@ static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, 
            static_cast<long long>(units), leaf_log2);
   leaves_kernel<M, T, DOT, VEC, NT><<<grid, NT, 0, stream>>>(
       px, py, ldx, ldy, rows, cols, leaf_log2, P, static_cast<Pair<A>*>(partials),
-      static_cast<unsigned*>(counters), static_cast<Pair<A>*>(out), fused);
+      static_cast<unsigned*>(counters), static_cast<Pair<A>*>(out), fused, part_cap);
   return check_launch();
 }
 
@@ -652,6 +658,9 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
                    (!DOT || (aligned16(y) && ((ldy * int64_t(sizeof(T))) % 16 == 0 || rows == 1)));
   auto px = static_cast<const T*>(x);
   auto py = static_cast<const T*>(y);
+  // partial-pair capacity the kernels may write: callers of the leaves-only mode
+  // (tf_reduce_leaves) promise ceil(n/L) pairs
+  const int64_t cap = fused ? (partial_capacity < 0 ? 0 : partial_capacity) : units;
   int S = choose_split(units, fused);
   // never exceed the scratch the caller provided (fused mode): S unit pairs per leaf
   // need rows*P*S partials, and any S*P > 1 needs the retire counters
@@ -661,9 +670,9 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
 
 #define TFB_NT(NT)                                                                                     \
   (vec ? launch_leaves_nt<M, T, DOT, true, NT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,   \
-                                               counters, out, fused, stream)                          \
+                                               counters, out, fused, stream, cap)                     \
        : launch_leaves_nt<M, T, DOT, false, NT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,  \
-                                                counters, out, fused, stream))
+                                                counters, out, fused, stream, cap))
   int loader = loader_choice();
   if (loader == 0) {
     const int64_t bytes = rows * cols * static_cast<int64_t>(sizeof(T)) * (DOT ? 2 : 1);
@@ -681,20 +690,20 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
   if (fused && tail != 1 && units * S > rows && partials && partial_capacity >= units * S) {
     int rc;
     if (S == 4) rc = (vec ? launch_leaves_nt<M, T, DOT, true, 64>(px, py, ldx, ldy, rows, cols, leaf_log2, P,
-                                                                   partials, nullptr, nullptr, 0, stream)
+                                                                   partials, nullptr, nullptr, 0, stream, partial_capacity)
                           : launch_leaves_nt<M, T, DOT, false, 64>(px, py, ldx, ldy, rows, cols, leaf_log2, P,
-                                                                    partials, nullptr, nullptr, 0, stream));
+                                                                    partials, nullptr, nullptr, 0, stream, partial_capacity));
     else if (S == 2) rc = (vec ? launch_leaves_nt<M, T, DOT, true, 128>(px, py, ldx, ldy, rows, cols, leaf_log2,
-                                                                         P, partials, nullptr, nullptr, 0, stream)
+                                                                         P, partials, nullptr, nullptr, 0, stream, partial_capacity)
                                : launch_leaves_nt<M, T, DOT, false, 128>(px, py, ldx, ldy, rows, cols, leaf_log2,
                                                                           P, partials, nullptr, nullptr, 0,
-                                                                          stream));
+                                                                          stream, partial_capacity));
     else rc = (vec ? launch_leaves_nt<M, T, DOT, true, 256>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,
-                                                             nullptr, nullptr, 0, stream)
+                                                             nullptr, nullptr, 0, stream, partial_capacity)
                    : launch_leaves_nt<M, T, DOT, false, 256>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,
-                                                              nullptr, nullptr, 0, stream));
+                                                              nullptr, nullptr, 0, stream, partial_capacity));
     if (rc) return rc;
-    return launch_rows_tree_pdl<M, typename Acc<M, T>::type>(partials, rows, P * S, out, stream);
+    return launch_rows_tree_pdl<M, typename Acc<M, T>::type>(partials, rows, P * S, out, stream, partial_capacity);
   }
   if (S == 4) return TFB_NT(64);
   if (S == 2) return TFB_NT(128);

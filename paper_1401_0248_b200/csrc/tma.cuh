@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) leaves_tma_kernel(
       for (int r0 = 0; r0 < R; r0 += SR) {
         const int nrow = R - r0 < SR ? R - r0 : SR;
         const uint32_t bytes = static_cast<uint32_t>(nrow * L::kRowVecs * sizeof(VT));
+        TFB_CHECK(static_cast<int64_t>(r0 + nrow) * L::kRowVecs * V <= Lelems && start + Lelems <= cols);
         mbar_wait(&empty[slot], phase ^ 1u);
         mbar_arrive_expect_tx(&full[slot], bytes * (DOT ? 2u : 1u));
         bulk_g2s(sx + slot * L::kStageVecs, gx + static_cast<int64_t>(r0) * L::kRowVecs * V, bytes, &full[slot]);

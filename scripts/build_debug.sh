@@ -1,0 +1,13 @@
+# Debug build of the library with device-side range/capacity assertions (TFB_DEBUG=1):
+# paper_1401_0248_b200/variants/libtwofold_b200_debug.so, used via TFB_LIB=<path>.
+set -e
+cd "$(dirname "$0")/../paper_1401_0248_b200/csrc"
+mkdir -p ../variants build_debug
+for f in reduce misc exact; do
+  nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -fmad=false -ftz=false -prec-div=true \
+    -prec-sqrt=true -lineinfo -Xcompiler -fPIC -I../../include -DTFB_DEBUG=1 -c $f.cu -o build_debug/$f.o &
+done
+wait
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o ../variants/libtwofold_b200_debug.so build_debug/*.o
+rm -rf build_debug
+echo built ../variants/libtwofold_b200_debug.so
