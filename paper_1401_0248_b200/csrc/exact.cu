@@ -37,7 +37,7 @@ struct ExactRecord {
   long long nonfinite;
 };
 
-__device__ __forceinline__ void deposit(long long* acc, double v) {
+__device__ __noinline__ void deposit(long long* acc, double v) {
   if (v == 0.0) return;
   const unsigned long long bits = __double_as_longlong(v);
   const bool neg = bits >> 63;
@@ -65,6 +65,13 @@ __device__ __forceinline__ void deposit(long long* acc, double v) {
 }
 
 __device__ __forceinline__ void cascade(double (&a)[kExpK], double x, long long* acc) {
+  // Keep every expansion component below 2^1001 so no TwoSum can overflow:
+  // huge addends (or a huge leading component) go straight to the fixed-point
+  // accumulator, which represents any finite sum of finite doubles exactly.
+  if (fabs(x) >= 0x1p1000 || fabs(a[0]) >= 0x1p1000) {
+    deposit(acc, x);
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < kExpK; ++i) {
     double s, e;
@@ -74,6 +81,16 @@ __device__ __forceinline__ void cascade(double (&a)[kExpK], double x, long long*
   }
   if (x != 0.0) deposit(acc, x);
 }
+
+template <typename T> struct ExVec;
+template <> struct ExVec<float> { using type = float4; static constexpr int V = 4; };
+template <> struct ExVec<double> { using type = double2; static constexpr int V = 2; };
+__device__ __forceinline__ float4 ex_ld(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ex_ld(const double2* p) { return __ldcs(p); }
+__device__ __forceinline__ float ex_get(const float4& v, int j) {
+  return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
+}
+__device__ __forceinline__ double ex_get(const double2& v, int j) { return j == 0 ? v.x : v.y; }
 
 // Addends: 0 = x_i, 1 = fl_T(x_i*y_i) (the twofold kernels' addends), 2 = exact
 // products (fl(x*y) and fma(x, y, -fl(x*y)) for binary64; exact in binary64 for
@@ -233,7 +250,7 @@ __device__ __noinline__ void finish(long long* tot, double* out, long long* limb
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kExactThreads) exact_kernel(
+__global__ void __launch_bounds__(kExactThreads, 4) exact_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t n, int mode, int absval,
     ExactRecord* __restrict__ records, unsigned* __restrict__ counter, double* __restrict__ out,
     long long* __restrict__ limbs_out) {
@@ -248,7 +265,44 @@ __global__ void __launch_bounds__(kExactThreads) exact_kernel(
   for (int i = 0; i < kExpK; ++i) a[i] = 0.0;
   int nonfinite = 0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += stride)
+  const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  // 16-byte vector loads, U vectors per operand in flight before the cascades
+  // run (the flush atomics keep the compiler from prefetching on its own).
+  using VT = typename ExVec<T>::type;
+  constexpr int VB = ExVec<T>::V;
+  constexpr int U = 2;
+  const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
+                       (y == nullptr || (reinterpret_cast<uintptr_t>(y) & 15u) == 0);
+  int64_t scalar_from = 0;
+  if (aligned) {
+    const int64_t nv = n / VB;
+    const VT* xv = reinterpret_cast<const VT*>(x);
+    const VT* yv = reinterpret_cast<const VT*>(y);
+    int64_t v = gtid;
+    for (; v + (U - 1) * stride < nv; v += U * stride) {
+      VT va[U], vb[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        va[k] = ex_ld(xv + v + k * stride);
+        if (y) vb[k] = ex_ld(yv + v + k * stride);
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+#pragma unroll
+        for (int j = 0; j < VB; ++j)
+          add_element<T>(a, acc, ex_get(va[k], j), y ? ex_get(vb[k], j) : T(0), mode, absval != 0, nonfinite);
+    }
+    for (; v < nv; v += stride) {
+      const VT va = ex_ld(xv + v);
+      VT vb;
+      if (y) vb = ex_ld(yv + v);
+#pragma unroll
+      for (int j = 0; j < VB; ++j)
+        add_element<T>(a, acc, ex_get(va, j), y ? ex_get(vb, j) : T(0), mode, absval != 0, nonfinite);
+    }
+    scalar_from = nv * VB;
+  }
+  for (int64_t i = scalar_from + gtid; i < n; i += stride)
     add_element<T>(a, acc, x[i], y ? y[i] : T(0), mode, absval != 0, nonfinite);
 #pragma unroll
   for (int i = 0; i < kExpK; ++i) deposit(acc, a[i]);

@@ -490,3 +490,13 @@ def test_pdl_tail_bit_identical(tfb, oracle, cuda):
     finally:
         L.tf_set_tail(0)
         L.tf_set_leaf_split(0)
+
+
+def test_gpu_exact_near_overflow(tfb, cuda):
+    """Partial sums beyond binary64 range stay exact in the superaccumulator."""
+    from fractions import Fraction
+    for x in (np.array([1e308, 1e308, -1e308, 5.0]), np.full(1000, 1.7e308), np.array([1e308] * 7 + [-1e308] * 7 + [1.0])):
+        got = tfb.exact_sum(x)
+        want = sum((Fraction(float(v)) for v in x), Fraction(0))
+        assert got.fraction() == want
+        assert got.hi == (float(want) if abs(want) < Fraction(2) ** 1024 else (np.inf if want > 0 else -np.inf))
