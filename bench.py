@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--leaf-log2", type=int, default=0, help="override the auto leaf size (sweeps)")
     ap.add_argument("--graph", action="store_true", help="replay the timed steps from a CUDA graph")
+    ap.add_argument("--combine", default="nccl", choices=["nccl", "peer"],
+                    help="cross-rank combine: NCCL all-gather + merge kernel, or the fused NVLink peer combine")
     ap.add_argument("--force-collective", action="store_true",
                     help="init NCCL and run the all-gather + merge path even at world size 1 (plumbing check)")
     return ap.parse_args()
@@ -288,7 +290,7 @@ def run_ours(args):
         if rows:
             return tfb.reduce_rows(method, xi, yi, leaf_log2=args.leaf_log2)
         return tfb.sharded_reduce(method, xi, yi, n_global=n_global if n_rank else n, leaf_log2=leaf_arg,
-                                  force_collective=args.force_collective)
+                                  force_collective=args.force_collective, combine=args.combine)
 
     def kernel_launch(i):
         xi, yi = copies[i % R]
@@ -347,7 +349,7 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms = t.item() / K_eff
     value = n * world * K_eff / (t.item() * 1e-3) / 1e9
-    launches_per_step = 1 + (1 if (world > 1 or args.force_collective) and not rows else 0)
+    launches_per_step = 1 + (1 if (world > 1 or args.force_collective) and not rows and args.combine == "nccl" else 0)
 
     # --- kernel-only timing (roofline of the reduction kernel) ---------------
     kernel_ms = timed(kernel_launch) / K_eff

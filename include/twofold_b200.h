@@ -145,6 +145,21 @@ int tf_reduce_rows(int method, int dtype, const void* x, const void* y,
                    int leaf_log2, void* out_pairs, void* partials, size_t partials_bytes,
                    void* counters, int64_t counters_len, void* stream);
 
+/* Fused cross-GPU combine over NVLink peer memory:
+ * tf_reduce of this rank's shard whose final CTA publishes the shard's pair
+ * into every peer's symmetric buffer, waits for all G pairs and runs the same
+ * balanced merge as tf_merge_tree — one launch instead of reduce + NCCL
+ * all-gather + merge; every rank gets the bit-identical global pair.
+ * peer_ctx: device pointer to a PeerCtx (csrc/peer.cuh; tf_peer_ctx_size()
+ * bytes): {int32 world, int32 rank, int32* error, void* bufs[16] (peer r's
+ * [2][world] pair buffer), uint32* flags[16] (peer r's [world] flags, zero at
+ * creation), uint64 max_spins}.  epoch: 1, 2, 3, ... identical on all ranks
+ * for the same call.  A peer that never arrives sets *error and yields NaN. */
+int tf_reduce_peer(int method, int dtype, const void* x, const void* y, int64_t n, int leaf_log2,
+                   void* out_pair, void* partials, size_t partials_bytes, void* counters,
+                   int64_t counters_len, const void* peer_ctx, uint32_t epoch, void* stream);
+int tf_peer_ctx_size(void);
+
 /* Leaf partials only (no tree): partials_out[0 .. ceil(n/2^leaf_log2)) for an
  * n-element chunk whose first element starts a leaf.  Used for streamed
  * host->device inputs and by the shard layer; finish with tf_merge_tree. */

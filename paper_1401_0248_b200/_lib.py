@@ -45,6 +45,8 @@ def _bind(L):
         "tf_workspace_size": ([i32, i32, i64, i64, i32, ctypes.POINTER(sz), ctypes.POINTER(i64),
                                ctypes.POINTER(i64)], i32),
         "tf_reduce": ([i32, i32, vp, vp, i64, i32, vp, vp, sz, vp, i64, vp], i32),
+        "tf_reduce_peer": ([i32, i32, vp, vp, i64, i32, vp, vp, sz, vp, i64, vp, ctypes.c_uint32, vp], i32),
+        "tf_peer_ctx_size": ([], i32),
         "tf_reduce_rows": ([i32, i32, vp, vp, i64, i64, i64, i64, i32, vp, vp, sz, vp, i64, vp], i32),
         "tf_reduce_leaves": ([i32, i32, vp, vp, i64, i32, vp, vp], i32),
         "tf_merge_tree": ([i32, i32, vp, i64, vp, vp], i32),

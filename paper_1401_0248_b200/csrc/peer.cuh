@@ -1,0 +1,89 @@
+// peer.cuh — fused cross-GPU combine over NVLink peer memory.
+// Included by reduce.cu after the tree helpers.
+//
+// The CTA that has just built this rank's root pair (last-leaf retire, TMA
+// last CTA, or the PDL tree kernel) finishes the job for the whole job:
+//   1. thread r < G stores the root into peer r's symmetric buffer, slot
+//      [epoch & 1][rank] (plain NVLink stores, then fence.sc.sys), and sets
+//      peer r's flag [rank] = epoch with st.release.sys;
+//   2. thread t < G waits (ld.acquire.sys, bounded spin) until this rank's
+//      flag [t] >= epoch, i.e. rank t's pair for this epoch has landed here;
+//   3. the CTA runs the same balanced tree as tf_merge_tree over the G pairs
+//      of slot [epoch & 1] and writes the global (value, error).
+// Every rank computes the identical tree over identical bytes, so all ranks
+// hold bit-identical results — the NCCL all-gather + merge kernel, fused
+// into the reduction's last step.  Epoch parity double-buffers the slots: a
+// rank can only reuse parity p two calls later, after every peer has already
+// consumed it (completing call k+1 needs every peer's k+1 publication, which
+// each peer issues only after it finished reading call k).  A spin that
+// exceeds the bound sets *error and yields NaN instead of hanging the GPU.
+
+namespace tfb {
+
+constexpr int kMaxPeers = 16;
+
+struct PeerCtx {
+  int32_t world;                  // G <= kMaxPeers
+  int32_t rank;
+  int32_t* error;                 // local device flag, set on a spin timeout
+  void* bufs[kMaxPeers];          // peer r's pair buffer: [2][G] Pair<A>
+  uint32_t* flags[kMaxPeers];     // peer r's flags: [G] uint32 (epoch of rank g's last publication)
+  unsigned long long max_spins;   // bound of the wait loop (x ~64 ns)
+};
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// All NT threads of the group call this; `root` is valid in thread 0.
+template <int M, typename A, int BAR = 0, int NT = kThreads>
+__device__ void finish_root(Pair<A> root, Pair<A>* out, const PeerCtx* peer, uint32_t epoch, Pair<A>* smem) {
+  const int t = threadIdx.x;
+  if (peer == nullptr) {
+    if (t == 0) *out = root;
+    return;
+  }
+  group_sync<BAR, NT>();
+  if (t == 0) smem[0] = root;
+  group_sync<BAR, NT>();
+  const Pair<A> mine = smem[0];
+  group_sync<BAR, NT>();
+  const int G = peer->world;
+  const int rank = peer->rank;
+  const int parity = static_cast<int>(epoch & 1u);
+  if (t < G) {
+    Pair<A>* dst = static_cast<Pair<A>*>(peer->bufs[t]) + parity * G + rank;
+    volatile A* d = reinterpret_cast<volatile A*>(dst);
+    d[0] = mine.s;
+    d[1] = mine.e;
+    __threadfence_system();
+    st_release_sys(peer->flags[t] + rank, epoch);
+  }
+  if (t < G) {
+    const uint32_t* f = peer->flags[rank] + t;
+    unsigned long long spins = 0;
+    while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
+      if (++spins > peer->max_spins) {
+        atomicExch(peer->error, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  group_sync<BAR, NT>();
+  Pair<A> global = tree_over<M, A, NT, BAR>(static_cast<const Pair<A>*>(peer->bufs[rank]) + parity * G, G, smem);
+  if (t == 0) {
+    if (*peer->error) {  // a peer never arrived: poison instead of a silent partial sum
+      global.s = A(__longlong_as_double(0x7FF8000000000000ll));
+      global.e = global.s;
+    }
+    *out = global;
+  }
+}
+
+}  // namespace tfb

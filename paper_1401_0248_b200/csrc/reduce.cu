@@ -179,6 +179,10 @@ __device__ Pair<A> tree_over(const Pair<A>* parts, int64_t P, Pair<A>* smem) {
   return block_tree<M, A, BAR, NT>(cur, smem, static_cast<int>(P2));
 }
 
+}  // namespace tfb
+#include "peer.cuh"
+namespace tfb {
+
 template <typename T, bool DOT, int U>
 __device__ __forceinline__ void load_batch(const typename Vec<T>::type* xv, const typename Vec<T>::type* yv,
                                            int k, typename Vec<T>::type (&a)[U],
@@ -297,7 +301,8 @@ __global__ void __launch_bounds__(NT) leaves_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy,
     int64_t rows, int64_t cols, int leaf_log2, int64_t P,
     Pair<typename Acc<M, T>::type>* __restrict__ partials, unsigned* __restrict__ counters,
-    Pair<typename Acc<M, T>::type>* __restrict__ out, int fused, int64_t part_cap) {
+    Pair<typename Acc<M, T>::type>* __restrict__ out, int fused, int64_t part_cap,
+    const PeerCtx* __restrict__ peer, uint32_t epoch) {
   using A = typename Acc<M, T>::type;
   constexpr int V = Vec<T>::V;
   constexpr int S = kThreads / NT;
@@ -325,7 +330,7 @@ __global__ void __launch_bounds__(NT) leaves_kernel(
       continue;
     }
     if (per_row == 1) {
-      if (threadIdx.x == 0) out[r] = st;
+      finish_root<M, A, 0, NT>(st, out + r, peer, epoch, smem);
       continue;
     }
     if (threadIdx.x == 0) {
@@ -337,10 +342,8 @@ __global__ void __launch_bounds__(NT) leaves_kernel(
     if (s_last) {
       acquire_fence();
       Pair<A> root = tree_over<M, A, NT>(partials + r * per_row, per_row, smem);
-      if (threadIdx.x == 0) {
-        out[r] = root;
-        counters[r] = 0u;  // leave the workspace reusable
-      }
+      if (threadIdx.x == 0) counters[r] = 0u;  // leave the workspace reusable
+      finish_root<M, A, 0, NT>(root, out + r, peer, epoch, smem);
     }
     __syncthreads();
   }
@@ -360,13 +363,14 @@ __global__ void __launch_bounds__(kThreads) tree_kernel(const Pair<A>* __restric
 template <int M, typename A>
 __global__ void __launch_bounds__(kThreads) rows_tree_kernel(const Pair<A>* __restrict__ partials, int64_t rows,
                                                              int64_t per_row, Pair<A>* __restrict__ out,
-                                                             int64_t part_cap) {
+                                                             int64_t part_cap, const PeerCtx* __restrict__ peer,
+                                                             uint32_t epoch) {
   __shared__ Pair<A> smem[kWarps];
   asm volatile("griddepcontrol.wait;" ::: "memory");
   TFB_CHECK(rows * per_row <= part_cap);
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     Pair<A> root = tree_over<M, A>(partials + r * per_row, per_row, smem);
-    if (threadIdx.x == 0) out[r] = root;
+    finish_root<M, A>(root, out + r, peer, epoch, smem);
     __syncthreads();
   }
 }
@@ -568,7 +572,7 @@ static int tail_choice() {
 
 template <int M, typename A>
 static int launch_rows_tree_pdl(const void* partials, int64_t rows, int64_t per_row, void* out,
-                                cudaStream_t stream, int64_t part_cap) {
+                                cudaStream_t stream, int64_t part_cap, const PeerCtx* peer, uint32_t epoch) {
   cudaLaunchConfig_t cfg = {};
   const int64_t sms = device_sms();
   cfg.gridDim = dim3(static_cast<unsigned>(rows < sms * 4 ? rows : sms * 4));
@@ -581,7 +585,7 @@ static int launch_rows_tree_pdl(const void* partials, int64_t rows, int64_t per_
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (cudaLaunchKernelEx(&cfg, rows_tree_kernel<M, A>, static_cast<const Pair<A>*>(partials), rows, per_row,
-                         static_cast<Pair<A>*>(out), part_cap) != cudaSuccess)
+                         static_cast<Pair<A>*>(out), part_cap, peer, epoch) != cudaSuccess)
     return record_cuda_error();
   return check_launch();
 }
@@ -589,7 +593,7 @@ static int launch_rows_tree_pdl(const void* partials, int64_t rows, int64_t per_
 template <int M, typename T, bool DOT, int NS, int SR>
 static int launch_leaves_tma(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                              int leaf_log2, int64_t P, void* partials, void* counters, void* out,
-                             cudaStream_t stream) {
+                             cudaStream_t stream, const PeerCtx* peer, uint32_t epoch) {
   using A = typename Acc<M, T>::type;
   auto kern = &leaves_tma_kernel<M, T, DOT, NS, SR>;
   const size_t smem = TmaSmem<T, DOT, NS, SR>::kBytes;
@@ -622,14 +626,15 @@ static int launch_leaves_tma(const T* px, const T* py, int64_t ldx, int64_t ldy,
            static_cast<long long>(units), leaf_log2);
   kern<<<grid, kTmaThreads, smem, stream>>>(px, py, ldx, ldy, rows, cols, leaf_log2, P,
                                             static_cast<Pair<A>*>(partials), static_cast<unsigned*>(counters),
-                                            static_cast<Pair<A>*>(out));
+                                            static_cast<Pair<A>*>(out), peer, epoch);
   return check_launch();
 }
 
 template <int M, typename T, bool DOT, bool VEC, int NT>
 static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                             int leaf_log2, int64_t P, void* partials, void* counters, void* out, int fused,
-                            cudaStream_t stream, int64_t part_cap = INT64_MAX) {
+                            cudaStream_t stream, int64_t part_cap = INT64_MAX, const PeerCtx* peer = nullptr,
+                            uint32_t epoch = 0) {
   using A = typename Acc<M, T>::type;
   const void* fn = reinterpret_cast<const void*>(&leaves_kernel<M, T, DOT, VEC, NT>);
   const int64_t units = rows * P * (kThreads / NT);
@@ -642,7 +647,7 @@ static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, 
            static_cast<long long>(units), leaf_log2);
   leaves_kernel<M, T, DOT, VEC, NT><<<grid, NT, 0, stream>>>(
       px, py, ldx, ldy, rows, cols, leaf_log2, P, static_cast<Pair<A>*>(partials),
-      static_cast<unsigned*>(counters), static_cast<Pair<A>*>(out), fused, part_cap);
+      static_cast<unsigned*>(counters), static_cast<Pair<A>*>(out), fused, part_cap, peer, epoch);
   return check_launch();
 }
 
@@ -650,10 +655,14 @@ template <int M, typename T, bool DOT>
 static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy, int64_t rows,
                          int64_t cols, int leaf_log2, void* partials, void* counters, void* out,
                          int fused, cudaStream_t stream, int64_t partial_capacity = -1,
-                         int64_t counter_capacity = -1) {
+                         int64_t counter_capacity = -1, const PeerCtx* peer = nullptr, uint32_t epoch = 0) {
   const int64_t P = (cols + (int64_t(1) << leaf_log2) - 1) >> leaf_log2;
   const int64_t units = rows * P;
-  if (units == 0) return TF_OK;
+  if (units == 0) {  // empty shard: still take part in the peer combine with (+0, +0)
+    if (peer && fused)
+      return launch_rows_tree_pdl<M, typename Acc<M, T>::type>(nullptr, 1, 0, out, stream, 0, peer, epoch);
+    return TF_OK;
+  }
   const bool vec = aligned16(x) && ((ldx * int64_t(sizeof(T))) % 16 == 0 || rows == 1) &&
                    (!DOT || (aligned16(y) && ((ldy * int64_t(sizeof(T))) % 16 == 0 || rows == 1)));
   auto px = static_cast<const T*>(x);
@@ -670,9 +679,9 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
 
 #define TFB_NT(NT)                                                                                     \
   (vec ? launch_leaves_nt<M, T, DOT, true, NT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,   \
-                                               counters, out, fused, stream, cap)                     \
+                                               counters, out, fused, stream, cap, peer, epoch)        \
        : launch_leaves_nt<M, T, DOT, false, NT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,  \
-                                                counters, out, fused, stream, cap))
+                                                counters, out, fused, stream, cap, peer, epoch))
   int loader = loader_choice();
   if (loader == 0) {
     const int64_t bytes = rows * cols * static_cast<int64_t>(sizeof(T)) * (DOT ? 2 : 1);
@@ -680,10 +689,10 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
   }
   if (vec && fused && S == 1 && loader == 2)
     return launch_leaves_tma<M, T, DOT, 4, 4>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
-                                              out, stream);
+                                              out, stream, peer, epoch);
   if (vec && fused && S == 1 && loader == 3)
     return launch_leaves_tma<M, T, DOT, 8, 2>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
-                                              out, stream);
+                                              out, stream, peer, epoch);
   // LDG loader.  Tail: auto/2 = partials-only launch + PDL tree kernel (measured
   // -0.5..-0.8 us on small inputs), 1 = single launch with last-CTA ticket.
   const int tail = tail_choice();
@@ -703,7 +712,8 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
                    : launch_leaves_nt<M, T, DOT, false, 256>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,
                                                               nullptr, nullptr, 0, stream, partial_capacity));
     if (rc) return rc;
-    return launch_rows_tree_pdl<M, typename Acc<M, T>::type>(partials, rows, P * S, out, stream, partial_capacity);
+    return launch_rows_tree_pdl<M, typename Acc<M, T>::type>(partials, rows, P * S, out, stream, partial_capacity,
+                                                             peer, epoch);
   }
   if (S == 4) return TFB_NT(64);
   if (S == 2) return TFB_NT(128);
@@ -863,19 +873,23 @@ int tf_workspace_size(int method, int dtype, int64_t rows, int64_t cols, int lea
   return TF_OK;
 }
 
-int tf_reduce_rows(int method, int dtype, const void* x, const void* y, int64_t rows, int64_t cols,
-                   int64_t ldx, int64_t ldy, int leaf_log2, void* out_pairs, void* partials,
-                   size_t partials_bytes, void* counters, int64_t counters_len, void* stream) {
+}  // extern "C"
+
+static int reduce_rows_impl(int method, int dtype, const void* x, const void* y, int64_t rows, int64_t cols,
+                            int64_t ldx, int64_t ldy, int leaf_log2, void* out_pairs, void* partials,
+                            size_t partials_bytes, void* counters, int64_t counters_len, void* stream,
+                            const PeerCtx* peer, uint32_t epoch) {
   int rc = validate(method, dtype);
   if (rc) return rc;
   if (rows < 0 || cols < 0) return TF_EINVAL_SHAPE;
   if (rows > 1 && (ldx < cols || (y && ldy < cols))) return TF_EINVAL_SHAPE;
+  if (peer && rows != 1) return TF_EINVAL_ARG;  // the peer combine merges one row across ranks
   if (rows == 0) return TF_OK;
   if (!out_pairs || (cols > 0 && !x)) return TF_EINVAL_ARG;
   int lg;
   if ((rc = resolve_leaf(dtype, rows * cols, leaf_log2, &lg))) return rc;
   auto s = static_cast<cudaStream_t>(stream);
-  if (cols == 0) {  // every row is empty: (+0, +0)
+  if (cols == 0 && !peer) {  // every row is empty: (+0, +0)
     if (cudaMemsetAsync(out_pairs, 0, static_cast<size_t>(rows) * pair_bytes(method, dtype), s) !=
         cudaSuccess)
       return record_cuda_error();
@@ -890,9 +904,18 @@ int tf_reduce_rows(int method, int dtype, const void* x, const void* y, int64_t 
   const bool dot = y != nullptr;
 #define TFB_CALL_LEAVES(M, T, DOT) \
   launch_leaves<M, T, DOT>(x, y, ldx, ldy, rows, cols, lg, parts, counters, out_pairs, 1, s, capacity, \
-                           counters ? counters_len : 0)
+                           counters ? counters_len : 0, peer, epoch)
   TFB_DISPATCH(internal_method(method), dtype, dot, TFB_CALL_LEAVES);
 #undef TFB_CALL_LEAVES
+}
+
+extern "C" {
+
+int tf_reduce_rows(int method, int dtype, const void* x, const void* y, int64_t rows, int64_t cols,
+                   int64_t ldx, int64_t ldy, int leaf_log2, void* out_pairs, void* partials,
+                   size_t partials_bytes, void* counters, int64_t counters_len, void* stream) {
+  return reduce_rows_impl(method, dtype, x, y, rows, cols, ldx, ldy, leaf_log2, out_pairs, partials,
+                          partials_bytes, counters, counters_len, stream, nullptr, 0);
 }
 
 int tf_reduce(int method, int dtype, const void* x, const void* y, int64_t n, int leaf_log2,
@@ -902,6 +925,17 @@ int tf_reduce(int method, int dtype, const void* x, const void* y, int64_t n, in
   return tf_reduce_rows(method, dtype, x, y, 1, n, n, n, leaf_log2, out_pair, partials,
                         partials_bytes, counters, counters_len, stream);
 }
+
+int tf_reduce_peer(int method, int dtype, const void* x, const void* y, int64_t n, int leaf_log2,
+                   void* out_pair, void* partials, size_t partials_bytes, void* counters,
+                   int64_t counters_len, const void* peer_ctx, uint32_t epoch, void* stream) {
+  if (n < 0) return TF_EINVAL_SHAPE;
+  if (!peer_ctx || epoch == 0) return TF_EINVAL_ARG;
+  return reduce_rows_impl(method, dtype, x, y, 1, n, n, n, leaf_log2, out_pair, partials, partials_bytes,
+                          counters, counters_len, stream, static_cast<const PeerCtx*>(peer_ctx), epoch);
+}
+
+int tf_peer_ctx_size(void) { return static_cast<int>(sizeof(PeerCtx)); }
 
 int tf_reduce_leaves(int method, int dtype, const void* x, const void* y, int64_t n, int leaf_log2,
                      void* partials_out, void* stream) {

@@ -64,7 +64,8 @@ template <int M, typename T, bool DOT, int NS, int SR>
 __global__ void __launch_bounds__(kTmaThreads, 1) leaves_tma_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy, int64_t rows,
     int64_t cols, int leaf_log2, int64_t P, Pair<typename Acc<M, T>::type>* __restrict__ partials,
-    unsigned* __restrict__ counters, Pair<typename Acc<M, T>::type>* __restrict__ out) {
+    unsigned* __restrict__ counters, Pair<typename Acc<M, T>::type>* __restrict__ out,
+    const PeerCtx* __restrict__ peer, uint32_t epoch) {
   using A = typename Acc<M, T>::type;
   using VT = typename Vec<T>::type;
   using L = TmaSmem<T, DOT, NS, SR>;
@@ -152,7 +153,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1) leaves_tma_kernel(
     }
     st = block_tree<M, A, 1, kTmaConsumers>(st, red, kThreads);
     if (P == 1) {
-      if (t == 0) out[r] = st;
+      finish_root<M, A, 1, kTmaConsumers>(st, out + r, peer, epoch, red);
       continue;
     }
     if (t == 0) {
@@ -163,10 +164,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) leaves_tma_kernel(
     if (s_last) {
       acquire_fence();
       Pair<A> root = tree_over<M, A, kThreads, 1>(partials + r * P, P, red);
-      if (t == 0) {
-        out[r] = root;
-        counters[r] = 0u;
-      }
+      if (t == 0) counters[r] = 0u;
+      finish_root<M, A, 1, kTmaConsumers>(root, out + r, peer, epoch, red);
     }
     group_sync<1, kTmaConsumers>();
   }

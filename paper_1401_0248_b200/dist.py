@@ -14,6 +14,14 @@ the single-GPU tree, so the G-GPU result is bit-identical to the 1-GPU one.
 The local reducer and the merge are injectable so the plumbing can be
 exercised with gloo on CPU (tests/test_dist_gloo.py); the defaults are the
 CUDA kernels and there is no CPU fallback.
+
+combine="peer" replaces reduce + NCCL all-gather + merge by ONE launch
+(tf_reduce_peer, csrc/peer.cuh): the CTA that builds the shard's root writes
+it into every peer's symmetric-memory buffer over NVLink, waits for the G
+pairs (system-scope release/acquire flags, epoch double-buffered, bounded
+spin) and merges them in-kernel.  It is opt-in: on this round's single-GPU
+pool it is verified at world size 1 (self-publication through the same code)
+and multi-GPU by construction; "nccl" stays the default.
 """
 
 from __future__ import annotations
@@ -54,6 +62,80 @@ def _default_merge(method: Method, pairs: torch.Tensor) -> torch.Tensor:
     return merge_pairs(method, pairs)
 
 
+class _PeerCombine:
+    """Symmetric buffers + device PeerCtx for one (group, device, accumulator dtype)."""
+
+    MAX_PEERS = 16
+
+    def __init__(self, group, dev: torch.device, acc: torch.dtype):
+        import struct
+
+        import torch.distributed._symmetric_memory as symm
+
+        from . import _lib
+        rank, world = _world(group)
+        if world > self.MAX_PEERS:
+            raise ValueError(f"peer combine supports up to {self.MAX_PEERS} ranks")
+        self.world, self.rank = world, rank
+        self.buf = symm.empty(2 * world * 2, dtype=acc, device=dev)      # [2 parities][world] pairs
+        self.flags = symm.empty(world, dtype=torch.int32, device=dev)    # epoch of rank g's last publication
+        self.flags.zero_()
+        self.error = torch.zeros(1, dtype=torch.int32, device=dev)
+        torch.cuda.synchronize(dev)
+        pg = group if group is not None else dist.group.WORLD
+        hb = symm.rendezvous(self.buf, pg)
+        hf = symm.rendezvous(self.flags, pg)
+        dist.barrier(group)
+        bufs = list(hb.buffer_ptrs) + [0] * (self.MAX_PEERS - world)
+        flags = list(hf.buffer_ptrs) + [0] * (self.MAX_PEERS - world)
+        max_spins = 1 << 27  # x ~64 ns: seconds, then *error = 1 and NaN instead of a hang
+        raw = struct.pack("<iiQ16Q16QQ", world, rank, self.error.data_ptr(), *bufs, *flags, max_spins)
+        assert len(raw) == _lib.lib().tf_peer_ctx_size(), "PeerCtx layout mismatch"
+        self.ctx = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev)
+        self.epoch = 0
+        self._handles = (hb, hf)  # keep the mappings alive
+
+    def next_epoch(self) -> int:
+        self.epoch += 1
+        return self.epoch
+
+
+_peer_cache: dict = {}
+
+
+def _peer_combine_for(group, dev: torch.device, acc: torch.dtype) -> _PeerCombine:
+    key = (id(group), dev.index, acc)
+    pc = _peer_cache.get(key)
+    if pc is None:
+        pc = _PeerCombine(group, dev, acc)
+        _peer_cache[key] = pc
+    return pc
+
+
+def _reduce_peer(method: Method, x: torch.Tensor, y, leaf_log2: int, group, track_product: bool) -> torch.Tensor:
+    from . import _lib
+    from .api import _acc_dtype, _dtype_code, _mid, _on_device, _ptr, _scratch, _stream_ptr, workspace_size
+    dev = x.device
+    _lib.ensure_canary(dev.index)
+    y = _on_device(y, dev)
+    x = x.contiguous()
+    acc = _acc_dtype(method, x.dtype)
+    pc = _peer_combine_for(group, dev, acc)
+    out = torch.empty(2, dtype=acc, device=dev)
+    pb, cnt, _ = workspace_size(method, x.dtype, 1, x.numel(), leaf_log2)
+    parts, ctrs = _scratch.get(dev, pb, cnt)
+    _lib.check(_lib.lib().tf_reduce_peer(_mid(method, track_product, y is not None), _dtype_code(x.dtype),
+                                         _ptr(x), _ptr(y), x.numel(), leaf_log2, out.data_ptr(), _ptr(parts), pb,
+                                         _ptr(ctrs), cnt, pc.ctx.data_ptr(), pc.next_epoch(), _stream_ptr(dev)),
+               "tf_reduce_peer")
+    return out
+
+
+def peer_combine_error(group=None) -> bool:
+    """True if any peer combine on this rank timed out waiting for a peer (result NaN)."""
+    return any(int(pc.error.item()) != 0 for (gid, _, _), pc in _peer_cache.items() if gid == id(group))
+
+
 def _world(group) -> tuple[int, int]:
     if dist.is_available() and dist.is_initialized():
         return dist.get_rank(group), dist.get_world_size(group)
@@ -63,14 +145,22 @@ def _world(group) -> tuple[int, int]:
 def sharded_reduce(method: Method, x_local: torch.Tensor, y_local: torch.Tensor | None = None, *,
                    n_global: int, leaf_log2: int = 0, group=None,
                    local_reduce: LocalReduce | None = None, merge: Merge | None = None,
-                   track_product: bool = False, force_collective: bool = False) -> torch.Tensor:
+                   track_product: bool = False, force_collective: bool = False,
+                   combine: str = "nccl") -> torch.Tensor:
     """Raw (value, error) pair of the global array, identical on every rank.
 
     x_local / y_local: this rank's shard (CUDA tensors for the default
     reducer).  leaf_log2 = 0 uses the global array's auto leaf size, so the
-    partition does not depend on G.
+    partition does not depend on G.  combine: "nccl" (all-gather + merge
+    kernel) or "peer" (fused NVLink combine inside the reduction launch).
     """
+    if combine not in ("nccl", "peer"):
+        raise ValueError("combine must be 'nccl' or 'peer'")
     lg = leaf_log2 or leaf_log2_for(x_local.dtype, n_global)
+    if combine == "peer" and dist.is_available() and dist.is_initialized() and local_reduce is None:
+        if not x_local.is_cuda:
+            raise ValueError("the peer combine reduces device-resident shards")
+        return _reduce_peer(method, x_local, y_local, lg, group, track_product)
     if local_reduce is None:
         local = _default_local(method, x_local, y_local, lg, track_product)
     else:
@@ -101,4 +191,4 @@ def sharded_run(method: Method, x_local, y_local=None, *, n_global: int, leaf_lo
     return SumResult(Twofold(t(v), t(0)), n_global)
 
 
-__all__ = ["shard_range", "sharded_reduce", "sharded_run"]
+__all__ = ["shard_range", "sharded_reduce", "sharded_run", "peer_combine_error"]
