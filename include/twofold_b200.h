@@ -193,6 +193,11 @@ int tf_reduce_lanes(int method, int dtype, const void* x, const void* y, int64_t
 int tf_noread(int method, int dtype, int dot, const void* seed8, int64_t iters, int64_t blocks,
               void* out_pairs, void* stream);
 
+/* Read roof (the paper's read1 / read2 rows): stream nbytes
+ * (16-byte aligned) with an XOR fold only, `unroll` (2/4/8/16) 16-byte loads in
+ * flight per thread, 8 CTAs x 256 threads per SM.  sink: one device uint32. */
+int tf_read_roof(const void* data, int64_t nbytes, int unroll, void* sink, void* stream);
+
 /* Elementwise EFTs on device arrays: kind 0 = fast_two_sum (eft.py:28-42),
  * kind 1 = two_sum (eft.py:45-56).  x_out = fl(a+b), y_out = round-off. */
 int tf_eft(int kind, int dtype, const void* a, const void* b, int64_t n,

@@ -54,6 +54,7 @@ def _bind(L):
         "tf_reduce_lanes": ([i32, i32, vp, vp, i64, i32, vp, vp], i32),
         "tf_eft": ([i32, i32, vp, vp, i64, vp, vp, vp], i32),
         "tf_fill": ([i32, i32, u64, u64, u64, i64, dbl, dbl, dbl, i64, vp, vp], i32),
+        "tf_read_roof": ([vp, i64, i32, vp, vp], i32),
         "tf_noread": ([i32, i32, i32, vp, i64, i64, vp, vp], i32),
         "tf_exact_workspace": ([ctypes.POINTER(i64), ctypes.POINTER(sz)], i32),
         "tf_exact": ([i32, vp, vp, i64, i32, vp, vp, vp, sz, vp, vp], i32),

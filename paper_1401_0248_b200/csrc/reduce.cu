@@ -693,6 +693,14 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
   if (vec && fused && S == 1 && loader == 3)
     return launch_leaves_tma<M, T, DOT, 8, 2>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
                                               out, stream, peer, epoch);
+  if constexpr (DOT) {  // experimental stage shapes for the large-dot case
+    if (vec && fused && S == 1 && loader == 4)
+      return launch_leaves_tma<M, T, DOT, 3, 8>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
+                                                out, stream, peer, epoch);
+    if (vec && fused && S == 1 && loader == 5)
+      return launch_leaves_tma<M, T, DOT, 6, 4>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
+                                                out, stream, peer, epoch);
+  }
   // LDG loader.  Tail: auto/2 = partials-only launch + PDL tree kernel (measured
   // -0.5..-0.8 us on small inputs), 1 = single launch with last-CTA ticket.
   const int tail = tail_choice();
@@ -842,7 +850,7 @@ int tf_set_tail(int tail) {
 }
 
 int tf_set_loader(int loader) {
-  if (loader < 0 || loader > 3) return TF_EINVAL_ARG;
+  if (loader < 0 || loader > 5) return TF_EINVAL_ARG;
   g_loader = loader;
   return TF_OK;
 }
