@@ -155,7 +155,8 @@ int tf_reduce_rows(int method, int dtype, const void* x, const void* y,
  * bytes): {int32 world, int32 rank, int32* error, void* bufs[16] (peer r's
  * [2][world] pair buffer), uint32* flags[16] (peer r's [world] flags, zero at
  * creation), uint64 max_spins}.  epoch: 1, 2, 3, ... identical on all ranks
- * for the same call.  A peer that never arrives sets *error and yields NaN. */
+ * for the same call.  A peer that never arrives sets *error and yields NaN.
+ * Unlike tf_reduce, the partials scratch is required even for a single leaf. */
 int tf_reduce_peer(int method, int dtype, const void* x, const void* y, int64_t n, int leaf_log2,
                    void* out_pair, void* partials, size_t partials_bytes, void* counters,
                    int64_t counters_len, const void* peer_ctx, uint32_t epoch, void* stream);

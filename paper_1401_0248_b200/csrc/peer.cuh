@@ -40,14 +40,13 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
-// All NT threads of the group call this; `root` is valid in thread 0.
-template <int M, typename A, int BAR = 0, int NT = kThreads>
-__device__ void finish_root(Pair<A> root, Pair<A>* out, const PeerCtx* peer, uint32_t epoch, Pair<A>* smem) {
+// Out of line: the combine runs once per launch and must not widen the hot
+// loop's register allocation (inlined, it cost leaves_kernel 14 registers and
+// one CTA per SM).
+template <int M, typename A, int BAR, int NT>
+__device__ __noinline__ void peer_finish(Pair<A> root, Pair<A>* out, const PeerCtx* peer, uint32_t epoch,
+                                         Pair<A>* smem) {
   const int t = threadIdx.x;
-  if (peer == nullptr) {
-    if (t == 0) *out = root;
-    return;
-  }
   group_sync<BAR, NT>();
   if (t == 0) smem[0] = root;
   group_sync<BAR, NT>();
@@ -84,6 +83,17 @@ __device__ void finish_root(Pair<A> root, Pair<A>* out, const PeerCtx* peer, uin
     }
     *out = global;
   }
+}
+
+// All NT threads of the group call this; `root` is valid in thread 0.
+template <int M, typename A, int BAR = 0, int NT = kThreads>
+__device__ __forceinline__ void finish_root(Pair<A> root, Pair<A>* out, const PeerCtx* peer, uint32_t epoch,
+                                            Pair<A>* smem) {
+  if (peer == nullptr) {
+    if (threadIdx.x == 0) *out = root;
+    return;
+  }
+  peer_finish<M, A, BAR, NT>(root, out, peer, epoch, smem);
 }
 
 }  // namespace tfb

@@ -301,8 +301,7 @@ __global__ void __launch_bounds__(NT) leaves_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy,
     int64_t rows, int64_t cols, int leaf_log2, int64_t P,
     Pair<typename Acc<M, T>::type>* __restrict__ partials, unsigned* __restrict__ counters,
-    Pair<typename Acc<M, T>::type>* __restrict__ out, int fused, int64_t part_cap,
-    const PeerCtx* __restrict__ peer, uint32_t epoch) {
+    Pair<typename Acc<M, T>::type>* __restrict__ out, int fused, int64_t part_cap) {
   using A = typename Acc<M, T>::type;
   constexpr int V = Vec<T>::V;
   constexpr int S = kThreads / NT;
@@ -330,7 +329,7 @@ __global__ void __launch_bounds__(NT) leaves_kernel(
       continue;
     }
     if (per_row == 1) {
-      finish_root<M, A, 0, NT>(st, out + r, peer, epoch, smem);
+      if (threadIdx.x == 0) out[r] = st;
       continue;
     }
     if (threadIdx.x == 0) {
@@ -342,8 +341,10 @@ __global__ void __launch_bounds__(NT) leaves_kernel(
     if (s_last) {
       acquire_fence();
       Pair<A> root = tree_over<M, A, NT>(partials + r * per_row, per_row, smem);
-      if (threadIdx.x == 0) counters[r] = 0u;  // leave the workspace reusable
-      finish_root<M, A, 0, NT>(root, out + r, peer, epoch, smem);
+      if (threadIdx.x == 0) {
+        out[r] = root;
+        counters[r] = 0u;  // leave the workspace reusable
+      }
     }
     __syncthreads();
   }
@@ -634,8 +635,7 @@ static int launch_leaves_tma(const T* px, const T* py, int64_t ldx, int64_t ldy,
 template <int M, typename T, bool DOT, bool VEC, int NT>
 static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                             int leaf_log2, int64_t P, void* partials, void* counters, void* out, int fused,
-                            cudaStream_t stream, int64_t part_cap = INT64_MAX, const PeerCtx* peer = nullptr,
-                            uint32_t epoch = 0) {
+                            cudaStream_t stream, int64_t part_cap = INT64_MAX) {
   using A = typename Acc<M, T>::type;
   const void* fn = reinterpret_cast<const void*>(&leaves_kernel<M, T, DOT, VEC, NT>);
   const int64_t units = rows * P * (kThreads / NT);
@@ -648,7 +648,7 @@ static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, 
            static_cast<long long>(units), leaf_log2);
   leaves_kernel<M, T, DOT, VEC, NT><<<grid, NT, 0, stream>>>(
       px, py, ldx, ldy, rows, cols, leaf_log2, P, static_cast<Pair<A>*>(partials),
-      static_cast<unsigned*>(counters), static_cast<Pair<A>*>(out), fused, part_cap, peer, epoch);
+      static_cast<unsigned*>(counters), static_cast<Pair<A>*>(out), fused, part_cap);
   return check_launch();
 }
 
@@ -680,9 +680,9 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
 
 #define TFB_NT(NT)                                                                                     \
   (vec ? launch_leaves_nt<M, T, DOT, true, NT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,   \
-                                               counters, out, fused, stream, cap, peer, epoch)        \
+                                               counters, out, fused, stream, cap)                     \
        : launch_leaves_nt<M, T, DOT, false, NT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,  \
-                                                counters, out, fused, stream, cap, peer, epoch))
+                                                counters, out, fused, stream, cap))
   int loader = loader_choice();
   if (loader == 0) {
     // measured (profiles/r01_summary.md, "Loader comparison" / "Sum loaders"):
@@ -712,7 +712,10 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
   // LDG loader.  Tail: auto/2 = partials-only launch + PDL tree kernel (measured
   // -0.5..-0.8 us on small inputs), 1 = single launch with last-CTA ticket.
   const int tail = tail_choice();
-  if (fused && tail != 1 && units * S > rows && partials && partial_capacity >= units * S) {
+  // The peer combine lives in the PDL tree kernel for the LDG loader (keeping it
+  // out of leaves_kernel keeps that kernel at 48 registers / 5 CTAs per SM).
+  if (peer && !(partials && partial_capacity >= units * S)) return TF_EWORKSPACE;
+  if (fused && (peer || (tail != 1 && units * S > rows)) && partials && partial_capacity >= units * S) {
     int rc;
     if (S == 4) rc = (vec ? launch_leaves_nt<M, T, DOT, true, 64>(px, py, ldx, ldy, rows, cols, leaf_log2, P,
                                                                    partials, nullptr, nullptr, 0, stream, partial_capacity)
