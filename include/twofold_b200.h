@@ -110,8 +110,8 @@ int tf_set_tail(int tail);
 const char* tf_last_launch(void);
 
 /* Tuning knob (process-wide): loader of the grid reduction for 16-byte aligned
- * inputs — 0 = automatic (default: TMA for >= 512 MiB dots and rigorous sums,
- * fast sums from 4 GiB, else LDG), 1 = 128-bit streaming LDG, 2 = warp-
+ * inputs — 0 = automatic (default: TMA for >= 512 MiB dots and >= 4 GiB
+ * twofold sums, else LDG), 1 = 128-bit streaming LDG, 2 = warp-
  * specialised bulk-copy (TMA engine) pipeline, 4 stages x 16 KiB per operand,
  * 3 = 8 x 8 KiB, 4 / 5 = experimental dot shapes (3 x 32 KiB, 6 x 16 KiB).
  * Results are bit-identical (same partition and trees); env TFB_LOADER sets

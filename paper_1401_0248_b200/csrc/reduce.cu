@@ -548,9 +548,9 @@ static int choose_split(int64_t units, int fused) {
 // 16 KiB per operand), 3 = TMA with 8 stages x 8 KiB, 4/5 = experimental dot
 // stage shapes (3 x 32 KiB, 6 x 16 KiB).  Results are identical.  Auto
 // (measured, profiles/r01_summary.md): TMA for >= 512 MiB dots (cfg5 +1.1 %,
-// cfg4 +2.5 %) and rigorous sums (cfg3 +5.8 %), fast sums from 4 GiB, LDG
-// otherwise (Kahan sums and mid/small sizes favour LDG's higher CTA
-// occupancy).  Env TFB_LOADER or tf_set_loader() override.
+// cfg4 +2.5 %) and >= 4 GiB twofold sums, LDG otherwise (Kahan sums and
+// mid/small sizes favour LDG's higher CTA occupancy).  Env TFB_LOADER or
+// tf_set_loader() override.
 static int g_loader = -1;
 static int loader_choice() {
   if (g_loader < 0) {
@@ -686,13 +686,12 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
   int loader = loader_choice();
   if (loader == 0) {
     // measured (profiles/r01_summary.md, "Loader comparison" / "Sum loaders"):
-    // the TMA pipeline wins for large dots and for the op-heavy rigorous sums
-    // (+4..12 %), fast sums only from ~4 GiB, Kahan sums prefer LDG
+    // the TMA pipeline wins for large dots and for >= 4 GiB twofold sums; at
+    // 1-2 GiB the sum results depend on power-cap state (short bursts favour
+    // LDG, sustained runs TMA), so LDG keeps them, and Kahan sums prefer LDG
     const int64_t bytes = rows * cols * static_cast<int64_t>(sizeof(T)) * (DOT ? 2 : 1);
-    constexpr bool rigorous = (M == kRigorous || M == kRigorousTP);
-    constexpr bool fast = (M == kFast || M == kFastTP);
-    const bool tma = bytes >= (int64_t(512) << 20) &&
-                     (DOT || rigorous || (fast && bytes >= (int64_t(4) << 30)));
+    constexpr bool twofold_sum = (M == kRigorous || M == kRigorousTP || M == kFast || M == kFastTP);
+    const bool tma = (DOT && bytes >= (int64_t(512) << 20)) || (twofold_sum && bytes >= (int64_t(4) << 30));
     loader = tma ? 2 : 1;
   }
   if (vec && fused && S == 1 && loader == 2)
