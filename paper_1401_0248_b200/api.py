@@ -307,14 +307,15 @@ def merge_pairs(method: Method, pairs: torch.Tensor, out: torch.Tensor | None = 
     """Balanced TwoSum/Kahan/plain tree over a (k, 2) device tensor of pairs."""
     pairs = pairs.contiguous()
     dev = pairs.device
-    if out is None:
-        out = torch.empty(2, dtype=pairs.dtype, device=dev)
-    data_dtype = torch.float32 if (pairs.dtype == torch.float32) else torch.float64
-    if method is Method.WIDE:
-        data_dtype = torch.float32
-    check(lib().tf_merge_tree(_METHOD_ID[method], _dtype_code(data_dtype), pairs.data_ptr(),
-                              pairs.numel() // 2, out.data_ptr(), _stream_ptr(dev)), "tf_merge_tree")
-    return out
+    with torch.cuda.device(dev):
+        if out is None:
+            out = torch.empty(2, dtype=pairs.dtype, device=dev)
+        data_dtype = torch.float32 if (pairs.dtype == torch.float32) else torch.float64
+        if method is Method.WIDE:
+            data_dtype = torch.float32
+        check(lib().tf_merge_tree(_METHOD_ID[method], _dtype_code(data_dtype), pairs.data_ptr(),
+                                  pairs.numel() // 2, out.data_ptr(), _stream_ptr(dev)), "tf_merge_tree")
+        return out
 
 
 _CHUNK_BYTES = 64 << 20  # per operand, per staging buffer
@@ -411,15 +412,16 @@ def reduce(method: Method, data, b=None, *, flavor: Flavor = _CUDA, leaf_log2: i
         raise TypeError("wide accumulation is defined for float32 data only")
     _mid(method, track_product, y is not None)  # validate before touching the device
     dev = _device_for(x)
-    if flavor.kind == "cuda":
-        if x.is_cuda:
-            return _reduce_grid(method, _on_device(x, dev), _on_device(y, dev), leaf_log2, out, track_product)
-        return _reduce_grid_host(method, x, y, dev, leaf_log2, track_product)
-    xd, yd = _on_device(x, dev), _on_device(y, dev)
-    if flavor.kind == "seq":
-        return _reduce_seq(method, xd, yd, dev, track_product)
-    k = flavor.lanes or _DEFAULT_LANES[np.dtype(_np_type(x.dtype))]
-    return _reduce_lanes(method, xd, yd, k, dev, track_product)
+    with torch.cuda.device(dev):  # the C library launches on the current device
+        if flavor.kind == "cuda":
+            if x.is_cuda:
+                return _reduce_grid(method, _on_device(x, dev), _on_device(y, dev), leaf_log2, out, track_product)
+            return _reduce_grid_host(method, x, y, dev, leaf_log2, track_product)
+        xd, yd = _on_device(x, dev), _on_device(y, dev)
+        if flavor.kind == "seq":
+            return _reduce_seq(method, xd, yd, dev, track_product)
+        k = flavor.lanes or _DEFAULT_LANES[np.dtype(_np_type(x.dtype))]
+        return _reduce_lanes(method, xd, yd, k, dev, track_product)
 
 
 def _finish(method: Method, pair: torch.Tensor, dtype: torch.dtype, n: int) -> SumResult:
@@ -534,21 +536,22 @@ def reduce_rows(method: Method, X, Y=None, *, leaf_log2: int = 0,
         raise TypeError("wide accumulation is defined for float32 data only")
     mid = _mid(method, track_product, y is not None)
     dev = _device_for(x)
-    if not x.is_cuda:
-        x = x.to(dev, non_blocking=x.is_pinned())
-    if y is not None and not y.is_cuda:
-        y = y.to(dev, non_blocking=y.is_pinned())
-    _lib.ensure_canary(dev.index)
-    rows, cols = x.shape
-    acc = _acc_dtype(method, x.dtype)
-    if out is None:
-        out = torch.empty(rows, 2, dtype=acc, device=dev)
-    pb, cnt, _ = workspace_size(method, x.dtype, rows, cols, leaf_log2)
-    parts, ctrs = _scratch.get(dev, pb, cnt)
-    check(lib().tf_reduce_rows(mid, _dtype_code(x.dtype), _ptr(x), _ptr(y), rows, cols,
-                               x.stride(0), 0 if y is None else y.stride(0), leaf_log2, out.data_ptr(),
-                               _ptr(parts), pb, _ptr(ctrs), cnt, _stream_ptr(dev)), "tf_reduce_rows")
-    return out
+    with torch.cuda.device(dev):
+        if not x.is_cuda:
+            x = x.to(dev, non_blocking=x.is_pinned())
+        if y is not None and not y.is_cuda:
+            y = y.to(dev, non_blocking=y.is_pinned())
+        _lib.ensure_canary(dev.index)
+        rows, cols = x.shape
+        acc = _acc_dtype(method, x.dtype)
+        if out is None:
+            out = torch.empty(rows, 2, dtype=acc, device=dev)
+        pb, cnt, _ = workspace_size(method, x.dtype, rows, cols, leaf_log2)
+        parts, ctrs = _scratch.get(dev, pb, cnt)
+        check(lib().tf_reduce_rows(mid, _dtype_code(x.dtype), _ptr(x), _ptr(y), rows, cols,
+                                   x.stride(0), 0 if y is None else y.stride(0), leaf_log2, out.data_ptr(),
+                                   _ptr(parts), pb, _ptr(ctrs), cnt, _stream_ptr(dev)), "tf_reduce_rows")
+        return out
 
 
 def _rows_result(method, pairs, cols) -> RowsResult:
@@ -587,13 +590,14 @@ def _eft(kind: int, a, b):
         raise TypeError(f"unsupported dtype {dt}")
     ta, tb = torch.broadcast_tensors(ta.to(dt), tb.to(dt))
     dev = _device_for(ta)
-    _lib.ensure_canary(dev.index)
-    ad = ta.to(dev).contiguous()
-    bd = tb.to(dev).contiguous()
-    xo = torch.empty_like(ad)
-    yo = torch.empty_like(ad)
-    check(lib().tf_eft(kind, _dtype_code(dt), ad.data_ptr(), bd.data_ptr(), ad.numel(), xo.data_ptr(),
-                       yo.data_ptr(), _stream_ptr(dev)), "tf_eft")
+    with torch.cuda.device(dev):
+        _lib.ensure_canary(dev.index)
+        ad = ta.to(dev).contiguous()
+        bd = tb.to(dev).contiguous()
+        xo = torch.empty_like(ad)
+        yo = torch.empty_like(ad)
+        check(lib().tf_eft(kind, _dtype_code(dt), ad.data_ptr(), bd.data_ptr(), ad.numel(), xo.data_ptr(),
+                           yo.data_ptr(), _stream_ptr(dev)), "tf_eft")
     if tens:
         return Twofold(xo, yo)
     xs, ys = xo.cpu().numpy(), yo.cpu().numpy()

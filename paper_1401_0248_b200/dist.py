@@ -52,14 +52,15 @@ def shard_range(n: int, rank: int, world: int, leaf_log2: int) -> tuple[int, int
 def _default_local(method: Method, x: torch.Tensor, y, leaf_log2: int, track_product: bool = False) -> torch.Tensor:
     from .api import _device_for, _on_device, _reduce_grid, _reduce_grid_host
     if x.is_cuda:
-        return _reduce_grid(method, x.contiguous(), _on_device(y, x.device), leaf_log2,
-                            track_product=track_product)
+        with torch.cuda.device(x.device):
+            return _reduce_grid(method, x.contiguous(), _on_device(y, x.device), leaf_log2,
+                                track_product=track_product)
     # host shard: leaf-aligned chunks streamed H2D, overlapped with the leaf kernels
     return _reduce_grid_host(method, x, y, _device_for(x), leaf_log2, track_product)
 
 
 def _default_merge(method: Method, pairs: torch.Tensor) -> torch.Tensor:
-    return merge_pairs(method, pairs)
+    return merge_pairs(method, pairs)  # enters pairs.device itself
 
 
 class _PeerCombine:
@@ -124,10 +125,12 @@ def _reduce_peer(method: Method, x: torch.Tensor, y, leaf_log2: int, group, trac
     out = torch.empty(2, dtype=acc, device=dev)
     pb, cnt, _ = workspace_size(method, x.dtype, 1, x.numel(), leaf_log2)
     parts, ctrs = _scratch.get(dev, pb, cnt)
-    _lib.check(_lib.lib().tf_reduce_peer(_mid(method, track_product, y is not None), _dtype_code(x.dtype),
-                                         _ptr(x), _ptr(y), x.numel(), leaf_log2, out.data_ptr(), _ptr(parts), pb,
-                                         _ptr(ctrs), cnt, pc.ctx.data_ptr(), pc.next_epoch(), _stream_ptr(dev)),
-               "tf_reduce_peer")
+    with torch.cuda.device(dev):
+        _lib.check(_lib.lib().tf_reduce_peer(_mid(method, track_product, y is not None), _dtype_code(x.dtype),
+                                             _ptr(x), _ptr(y), x.numel(), leaf_log2, out.data_ptr(), _ptr(parts),
+                                             pb, _ptr(ctrs), cnt, pc.ctx.data_ptr(), pc.next_epoch(),
+                                             _stream_ptr(dev)),
+                   "tf_reduce_peer")
     return out
 
 

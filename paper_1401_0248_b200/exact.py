@@ -67,17 +67,18 @@ _ws = _Ws()
 
 def _exact(x: torch.Tensor, y: torch.Tensor | None, flags: int) -> ExactValue:
     dev = _device_for(x)
-    x = _on_device(x, dev)
-    y = _on_device(y, dev)
-    _lib.ensure_canary(dev.index)
-    recs, nbytes = ctypes.c_int64(0), ctypes.c_size_t(0)
-    check(lib().tf_exact_workspace(ctypes.byref(recs), ctypes.byref(nbytes)), "tf_exact_workspace")
-    buf, counter = _ws.get(dev, nbytes.value)
-    out = torch.empty(2, dtype=torch.float64, device=dev)
-    limbs = torch.empty(_LIMBS + 1, dtype=torch.int64, device=dev)
-    check(lib().tf_exact(_dtype_code(x.dtype), x.data_ptr(), None if y is None else y.data_ptr(), x.numel(),
-                         flags, out.data_ptr(), limbs.data_ptr(), buf.data_ptr(), nbytes.value,
-                         counter.data_ptr(), _stream_ptr(dev)), "tf_exact")
+    with torch.cuda.device(dev):
+        x = _on_device(x, dev)
+        y = _on_device(y, dev)
+        _lib.ensure_canary(dev.index)
+        recs, nbytes = ctypes.c_int64(0), ctypes.c_size_t(0)
+        check(lib().tf_exact_workspace(ctypes.byref(recs), ctypes.byref(nbytes)), "tf_exact_workspace")
+        buf, counter = _ws.get(dev, nbytes.value)
+        out = torch.empty(2, dtype=torch.float64, device=dev)
+        limbs = torch.empty(_LIMBS + 1, dtype=torch.int64, device=dev)
+        check(lib().tf_exact(_dtype_code(x.dtype), x.data_ptr(), None if y is None else y.data_ptr(), x.numel(),
+                             flags, out.data_ptr(), limbs.data_ptr(), buf.data_ptr(), nbytes.value,
+                             counter.data_ptr(), _stream_ptr(dev)), "tf_exact")
     hi, lo = out.cpu().tolist()
     return ExactValue(hi, lo, tuple(limbs.cpu().tolist()))
 

@@ -23,7 +23,8 @@ _DIST = {"uniform01": _lib.DIST_UNIFORM01, "uniform_sym": _lib.DIST_UNIFORM_SYM,
 def _dev(device) -> torch.device:
     if device is None:
         return torch.device("cuda", torch.cuda.current_device())
-    return torch.device(device)
+    d = torch.device(device)
+    return d if d.index is not None else torch.device("cuda", torch.cuda.current_device())
 
 
 def philox_fill(dist: str, n: int, *, seed: int, stream: int = 0, offset: int = 0,
@@ -40,8 +41,9 @@ def philox_fill(dist: str, n: int, *, seed: int, stream: int = 0, offset: int = 
         out = torch.empty(n, dtype=dtype, device=dev)
     code = _lib.TF_F32 if out.dtype == torch.float32 else _lib.TF_F64
     tot = total if total is not None else offset + n
-    check(lib().tf_fill(_DIST[dist], code, seed, stream, offset, n, params[0], params[1], params[2], tot,
-                        out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream), "tf_fill")
+    with torch.cuda.device(dev):
+        check(lib().tf_fill(_DIST[dist], code, seed, stream, offset, n, params[0], params[1], params[2], tot,
+                            out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream), "tf_fill")
     return out
 
 
@@ -71,8 +73,9 @@ def lcg_fill(kind: str, n: int, seed: int = 1, dtype: torch.dtype = torch.float6
     if out is None:
         out = torch.empty(n, dtype=dtype, device=dev)
     code = _lib.TF_F32 if out.dtype == torch.float32 else _lib.TF_F64
-    check(lib().tf_lcg_fill(0 if kind == "nr" else 1, code, seed, 1 if sym else 0, offset, n, out.data_ptr(),
-                            torch.cuda.current_stream(dev).cuda_stream), "tf_lcg_fill")
+    with torch.cuda.device(dev):
+        check(lib().tf_lcg_fill(0 if kind == "nr" else 1, code, seed, 1 if sym else 0, offset, n, out.data_ptr(),
+                                torch.cuda.current_stream(dev).cuda_stream), "tf_lcg_fill")
     return out
 
 
@@ -84,9 +87,10 @@ def rows_scaled_normal(rows: int, cols: int, *, seed: int, stream: int, scale_st
     dev = _dev(device)
     out = torch.empty(rows, cols, dtype=dtype, device=dev)
     code = _lib.TF_F32 if dtype == torch.float32 else _lib.TF_F64
-    check(lib().tf_fill_rows_scaled(code, seed, stream, scale_stream, row0, rows, cols, cols, lo, hi,
-                                    out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
-          "tf_fill_rows_scaled")
+    with torch.cuda.device(dev):
+        check(lib().tf_fill_rows_scaled(code, seed, stream, scale_stream, row0, rows, cols, cols, lo, hi,
+                                        out.data_ptr(), torch.cuda.current_stream(dev).cuda_stream),
+              "tf_fill_rows_scaled")
     return out
 
 
