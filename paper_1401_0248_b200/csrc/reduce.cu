@@ -296,7 +296,7 @@ template <> struct Unroll<double> { static constexpr int value = TFB_UNROLL_F64;
 // not depend on S — S only balances the grid over the SMs.
 // mode 0: write unit pairs to partials[u] only.  mode 1: fused — the CTA that
 // retires a row's last unit builds the row tree into out[r].
-template <int M, typename T, bool DOT, bool VEC, int NT>
+template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1>
 __global__ void __launch_bounds__(NT) leaves_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy,
     int64_t rows, int64_t cols, int leaf_log2, int64_t P,
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(NT) leaves_kernel(
     const int part = static_cast<int>(rem - l * S);
     const T* xr = x + r * ldx;
     const T* yr = DOT ? y + r * ldy : nullptr;
-    Pair<A> st = leaf_chain<M, T, DOT, VEC, Unroll<T>::value>(
+    Pair<A> st = leaf_chain<M, T, DOT, VEC, Unroll<T>::value * UF>(
         xr, yr, l << leaf_log2, cols, R, part * NT + static_cast<int>(threadIdx.x));
     st = block_tree<M, A>(st, smem, NT);
     if (!fused) {
@@ -551,6 +551,20 @@ static int choose_split(int64_t units, int fused) {
 // cfg4 +2.5 %) and >= 4 GiB twofold sums, LDG otherwise (Kahan sums and
 // mid/small sizes favour LDG's higher CTA occupancy).  Env TFB_LOADER or
 // tf_set_loader() override.
+// Measured loader table (scripts/tune_loaders.py writes loader_table.inc):
+// best loader per (f64, dot, method class, floor(log2(bytes)) in [20, 33]).
+// Method classes: 0 direct/wide, 1 twofold-fast(+TP), 2 twofold-rigorous(+TP), 3 kahan.
+#include "loader_table.inc"
+
+static int auto_loader(int M, bool f64, bool dot, int64_t bytes) {
+  const int mclass = (M == kFast || M == kFastTP) ? 1 : (M == kRigorous || M == kRigorousTP) ? 2 : M == kKahan ? 3 : 0;
+  int b = 0;
+  while ((int64_t(2) << b) <= bytes && b < 62) ++b;  // floor(log2(bytes))
+  if (b < kLoaderTableMinLog2) return 1;
+  if (b > kLoaderTableMaxLog2) b = kLoaderTableMaxLog2;
+  return kLoaderTable[f64 ? 1 : 0][dot ? 1 : 0][mclass][b - kLoaderTableMinLog2];
+}
+
 static int g_loader = -1;
 static int loader_choice() {
   if (g_loader < 0) {
@@ -592,12 +606,12 @@ static int launch_rows_tree_pdl(const void* partials, int64_t rows, int64_t per_
   return check_launch();
 }
 
-template <int M, typename T, bool DOT, int NS, int SR>
+template <int M, typename T, bool DOT, int NS, int SR, int MINB = 1>
 static int launch_leaves_tma(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                              int leaf_log2, int64_t P, void* partials, void* counters, void* out,
                              cudaStream_t stream, const PeerCtx* peer, uint32_t epoch) {
   using A = typename Acc<M, T>::type;
-  auto kern = &leaves_tma_kernel<M, T, DOT, NS, SR>;
+  auto kern = &leaves_tma_kernel<M, T, DOT, NS, SR, MINB>;
   const size_t smem = TmaSmem<T, DOT, NS, SR>::kBytes;
   static std::mutex mu;
   static std::unordered_map<int, int> occ;  // per device
@@ -632,21 +646,22 @@ static int launch_leaves_tma(const T* px, const T* py, int64_t ldx, int64_t ldy,
   return check_launch();
 }
 
-template <int M, typename T, bool DOT, bool VEC, int NT>
+template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1>
 static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                             int leaf_log2, int64_t P, void* partials, void* counters, void* out, int fused,
                             cudaStream_t stream, int64_t part_cap = INT64_MAX) {
   using A = typename Acc<M, T>::type;
-  const void* fn = reinterpret_cast<const void*>(&leaves_kernel<M, T, DOT, VEC, NT>);
+  const void* fn = reinterpret_cast<const void*>(&leaves_kernel<M, T, DOT, VEC, NT, UF>);
   const int64_t units = rows * P * (kThreads / NT);
   const int64_t slots = static_cast<int64_t>(device_sms()) * occupancy_of(fn, NT);
   const int64_t grid64 = units < slots ? units : slots;
   const unsigned grid = static_cast<unsigned>(grid64 > 0 ? grid64 : 1);
   snprintf(g_last_launch, sizeof(g_last_launch),
-           "leaves_kernel<%s,%s,%s,%s,NT=%d> grid=%u block=%d units=%lld leaf_log2=%d", method_tag(M),
-           sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", VEC ? "ldg128" : "scalar", NT, grid, NT,
+           "leaves_kernel<%s,%s,%s,%s,NT=%d,U=%d> grid=%u block=%d units=%lld leaf_log2=%d", method_tag(M),
+           sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", VEC ? "ldg128" : "scalar", NT,
+           Unroll<T>::value * UF, grid, NT,
            static_cast<long long>(units), leaf_log2);
-  leaves_kernel<M, T, DOT, VEC, NT><<<grid, NT, 0, stream>>>(
+  leaves_kernel<M, T, DOT, VEC, NT, UF><<<grid, NT, 0, stream>>>(
       px, py, ldx, ldy, rows, cols, leaf_log2, P, static_cast<Pair<A>*>(partials),
       static_cast<unsigned*>(counters), static_cast<Pair<A>*>(out), fused, part_cap);
   return check_launch();
@@ -684,30 +699,26 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
        : launch_leaves_nt<M, T, DOT, false, NT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,  \
                                                 counters, out, fused, stream, cap))
   int loader = loader_choice();
-  if (loader == 0) {
-    // measured (profiles/r01_summary.md, "Loader comparison" / "Sum loaders"):
-    // the TMA pipeline wins for large dots and for >= 4 GiB twofold sums; at
-    // 1-2 GiB the sum results depend on power-cap state (short bursts favour
-    // LDG, sustained runs TMA), so LDG keeps them, and Kahan sums prefer LDG
-    const int64_t bytes = rows * cols * static_cast<int64_t>(sizeof(T)) * (DOT ? 2 : 1);
-    constexpr bool twofold_sum = (M == kRigorous || M == kRigorousTP || M == kFast || M == kFastTP);
-    const bool tma = (DOT && bytes >= (int64_t(512) << 20)) || (twofold_sum && bytes >= (int64_t(4) << 30));
-    loader = tma ? 2 : 1;
+  if (loader == 0) loader = auto_loader(M, sizeof(T) == 8, DOT, rows * cols * static_cast<int64_t>(sizeof(T)) * (DOT ? 2 : 1));
+  if (vec && fused && S == 1) {
+    switch (loader) {
+      case 2:
+        return launch_leaves_tma<M, T, DOT, 4, 4>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
+                                                  out, stream, peer, epoch);
+      case 3:
+        return launch_leaves_tma<M, T, DOT, 8, 2>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
+                                                  out, stream, peer, epoch);
+      case 6:  // small rings, 4 CTAs per SM
+        return launch_leaves_tma<M, T, DOT, 4, 1, 4>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,
+                                                     counters, out, stream, peer, epoch);
+      case 7:  // small rings, 3 CTAs per SM
+        return launch_leaves_tma<M, T, DOT, 4, 2, 3>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,
+                                                     counters, out, stream, peer, epoch);
+      default:
+        break;
+    }
   }
-  if (vec && fused && S == 1 && loader == 2)
-    return launch_leaves_tma<M, T, DOT, 4, 4>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
-                                              out, stream, peer, epoch);
-  if (vec && fused && S == 1 && loader == 3)
-    return launch_leaves_tma<M, T, DOT, 8, 2>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
-                                              out, stream, peer, epoch);
-  if constexpr (DOT) {  // experimental stage shapes for the large-dot case
-    if (vec && fused && S == 1 && loader == 4)
-      return launch_leaves_tma<M, T, DOT, 3, 8>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
-                                                out, stream, peer, epoch);
-    if (vec && fused && S == 1 && loader == 5)
-      return launch_leaves_tma<M, T, DOT, 6, 4>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
-                                                out, stream, peer, epoch);
-  }
+  const bool deep = vec && S == 1 && loader == 8;  // LDG with twice the loads in flight per thread
   // LDG loader.  Tail: auto/2 = partials-only launch + PDL tree kernel (measured
   // -0.5..-0.8 us on small inputs), 1 = single launch with last-CTA ticket.
   const int tail = tail_choice();
@@ -725,6 +736,9 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
                                : launch_leaves_nt<M, T, DOT, false, 128>(px, py, ldx, ldy, rows, cols, leaf_log2,
                                                                           P, partials, nullptr, nullptr, 0,
                                                                           stream, partial_capacity));
+    else if (deep) rc = launch_leaves_nt<M, T, DOT, true, 256, 2>(px, py, ldx, ldy, rows, cols, leaf_log2, P,
+                                                                  partials, nullptr, nullptr, 0, stream,
+                                                                  partial_capacity);
     else rc = (vec ? launch_leaves_nt<M, T, DOT, true, 256>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,
                                                              nullptr, nullptr, 0, stream, partial_capacity)
                    : launch_leaves_nt<M, T, DOT, false, 256>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,
@@ -735,6 +749,9 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
   }
   if (S == 4) return TFB_NT(64);
   if (S == 2) return TFB_NT(128);
+  if (deep)
+    return launch_leaves_nt<M, T, DOT, true, 256, 2>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
+                                                     out, fused, stream, cap);
   return TFB_NT(256);
 #undef TFB_NT
 }
@@ -860,7 +877,7 @@ int tf_set_tail(int tail) {
 }
 
 int tf_set_loader(int loader) {
-  if (loader < 0 || loader > 5) return TF_EINVAL_ARG;
+  if (loader < 0 || loader > 8 || loader == 4 || loader == 5) return TF_EINVAL_ARG;
   g_loader = loader;
   return TF_OK;
 }

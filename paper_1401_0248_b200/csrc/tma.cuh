@@ -60,8 +60,8 @@ struct TmaSmem {
   static constexpr size_t kBytes = NS * kStageBytes * (DOT ? 2 : 1) + 2 * NS * sizeof(uint64_t) + 64;
 };
 
-template <int M, typename T, bool DOT, int NS, int SR>
-__global__ void __launch_bounds__(kTmaThreads, 1) leaves_tma_kernel(
+template <int M, typename T, bool DOT, int NS, int SR, int MINB = 1>
+__global__ void __launch_bounds__(kTmaThreads, MINB) leaves_tma_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy, int64_t rows,
     int64_t cols, int leaf_log2, int64_t P, Pair<typename Acc<M, T>::type>* __restrict__ partials,
     unsigned* __restrict__ counters, Pair<typename Acc<M, T>::type>* __restrict__ out,

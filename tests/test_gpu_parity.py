@@ -449,14 +449,14 @@ def test_tma_loader_bit_identical(tfb, oracle, cuda):
                     meth = list(tfb.Method)[m]
                     for yy, yyh in ((None, None), (y, yh)):
                         want = oracle.emulate(m, xh, yyh)
-                        for loader in (1, 2, 3):
+                        for loader in (1, 2, 3, 6, 7):
                             assert L.tf_set_loader(loader) == 0
                             _same(tfb.reduce(meth, x, yy).cpu().numpy(), want, (dt, n, m, loader))
             X = tfb.rows_scaled_normal(33, 70_000, seed=5, stream=0, dtype=torch.float32)
             Y = tfb.rows_scaled_normal(33, 70_000, seed=5, stream=1, dtype=torch.float32)
             L.tf_set_loader(1)
             ref = tfb.reduce_rows(tfb.Method.TWOFOLD_FAST, X, Y).cpu()
-            for loader in (0, 2, 3):
+            for loader in (0, 2, 3, 6, 7):
                 L.tf_set_loader(loader)
                 assert torch.equal(tfb.reduce_rows(tfb.Method.TWOFOLD_FAST, X, Y).cpu(), ref)
     finally:

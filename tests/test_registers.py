@@ -32,7 +32,7 @@ def regs():
 
 def test_ldg_leaves_kernels_keep_five_ctas_per_sm(regs):
     # leaves_kernel<M, T, DOT, VEC=1, NT=256>: <= 51 registers -> 5 CTAs x 256 threads per SM
-    vec256 = {f: r for f, r in regs.items() if re.search(r"leaves_kernelILi[0-6]E[fd]Lb[01]ELb1ELi256E", f)}
+    vec256 = {f: r for f, r in regs.items() if re.search(r"leaves_kernelILi[0-6]E[fd]Lb[01]ELb1ELi256ELi1E", f)}
     assert len(vec256) >= 19
     over = {f: r for f, r in vec256.items() if r > 51}
     # the rigorous/TwoProduct f64 dots are allowed up to 64 (4 CTAs/SM); everything else 5
@@ -43,3 +43,10 @@ def test_ldg_leaves_kernels_keep_five_ctas_per_sm(regs):
 def test_tma_kernels_fit_one_cta_per_sm(regs):
     tma = {f: r for f, r in regs.items() if "leaves_tma_kernel" in f}
     assert tma and max(tma.values()) <= 224  # 288 threads x 224 <= 65536
+
+
+def test_deep_ldg_variants_keep_four_ctas_per_sm(regs):
+    # leaves_kernel<..., NT=256, UF=2>: twice the loads in flight, <= 64 registers (4 CTAs/SM)
+    deep = {f: r for f, r in regs.items() if re.search(r"leaves_kernelILi[0-6]E[fd]Lb[01]ELb1ELi256ELi2E", f)}
+    assert len(deep) >= 19
+    assert max(deep.values()) <= 64, {f: r for f, r in deep.items() if r > 64}
