@@ -699,7 +699,12 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
        : launch_leaves_nt<M, T, DOT, false, NT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,  \
                                                 counters, out, fused, stream, cap))
   int loader = loader_choice();
-  if (loader == 0) loader = auto_loader(M, sizeof(T) == 8, DOT, rows * cols * static_cast<int64_t>(sizeof(T)) * (DOT ? 2 : 1));
+  if (loader == 0) {
+    const int64_t bytes = rows * cols * static_cast<int64_t>(sizeof(T)) * (DOT ? 2 : 1);
+    // the table is measured on 1-D arrays; the row family (one unit per short row)
+    // streams best with the TMA pipeline once it is large (cfg4: 295 vs 303 us)
+    loader = (rows > 1 && DOT && bytes >= (int64_t(512) << 20)) ? 2 : auto_loader(M, sizeof(T) == 8, DOT, bytes);
+  }
   if (vec && fused && S == 1) {
     switch (loader) {
       case 2:
