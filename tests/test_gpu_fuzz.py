@@ -1,0 +1,73 @@
+"""Randomised parity: GPU grid flavor == the oracle's restatement of the tree, bit
+for bit, over random (method, precision, sum/dot, n, leaf size, misalignment,
+loader, tail, leaf split, TwoProduct); plus the reference's small-instance
+criterion C6 (test_acceptance.py:180-204) on the GPU tree."""
+
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tfb(cuda):
+    import paper_1401_0248_b200 as m
+    torch.cuda.set_device(cuda)
+    return m
+
+
+def test_fuzz_grid_vs_emulator(tfb, oracle, cuda):
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    rng = np.random.default_rng(20261020)
+    try:
+        for case in range(300):
+            dt = np.float32 if rng.random() < 0.5 else np.float64
+            methods = (0, 1, 2, 3, 4) if dt == np.float32 else (0, 2, 3, 4)
+            m = int(rng.choice(methods))
+            dot = bool(rng.random() < 0.6)
+            tp = dot and m in (2, 3) and rng.random() < 0.3
+            n = int(rng.choice([rng.integers(0, 64), rng.integers(64, 5000), rng.integers(5000, 300_000),
+                                rng.integers(300_000, 2_000_000)]))
+            off = int(rng.integers(0, 3))
+            lo = 10 if dt == np.float32 else 9
+            lg = int(rng.choice([0, 0, rng.integers(lo, 18)]))
+            scale = 2.0 ** rng.integers(-30, 30)
+            xh = (rng.standard_normal(n + off) * scale * 2.0 ** rng.integers(-8, 8, n + off)).astype(dt)
+            yh = rng.uniform(-1, 1, n + off).astype(dt)
+            x, y = torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda)
+            L.tf_set_loader(int(rng.choice([0, 1, 2, 3, 6, 7, 8])))
+            L.tf_set_tail(int(rng.choice([0, 1, 2])))
+            L.tf_set_leaf_split(int(rng.choice([0, 1, 2, 4])))
+            meth = list(tfb.Method)[m]
+            got = tfb.reduce(meth, x[off:], y[off:] if dot else None, leaf_log2=lg, track_product=tp).cpu().numpy()
+            want = oracle.emulate(m + (3 if tp else 0), xh[off:], yh[off:] if dot else None, lg)
+            assert float(got[0]).hex() == float(want[0]).hex() and float(got[1]).hex() == float(want[1]).hex(), \
+                (case, dt, m, dot, tp, n, off, lg, got, want)
+    finally:
+        L.tf_set_loader(0)
+        L.tf_set_tail(0)
+        L.tf_set_leaf_split(0)
+
+
+def test_small_instance_criterion_c6_on_the_grid(tfb, oracle):
+    """|v + e - S| <= 2 eps |S| for the rigorous grid flavor on the reference's C6 instances."""
+    def check(data, eps):
+        r = tfb.sum_twofold_rigorous(data)
+        got = Fraction(float(r.value)) + Fraction(float(r.error))
+        exact = sum((Fraction(float(v)) for v in data), Fraction(0))
+        assert abs(got - exact) <= 2 * Fraction(eps) * abs(exact), (data, r)
+
+    mags = [1.0, 2.0 ** -24, 3.25, 7.1e-3, 2.0 ** 20]
+    for bits in range(32):
+        signed = [(-m if bits >> i & 1 else m) for i, m in enumerate(mags)]
+        check(np.array(signed, np.float64), 2.0 ** -53)
+        check(np.array(signed, np.float32), 2.0 ** -24)
+    rng = np.random.default_rng(6)
+    for _ in range(300):
+        n = int(rng.integers(1, 21))
+        data = (rng.uniform(-1, 1, n) * 2.0 ** rng.integers(-8, 8, n))
+        check(data.astype(np.float32), 2.0 ** -24)
