@@ -18,6 +18,19 @@ if REPO not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and the built .so")
     config.addinivalue_line("markers", "slow: large CPU-side oracle work")
+    _ensure_built()
+
+
+def _ensure_built():
+    """Built libraries are git-ignored: build them once if a fresh checkout lacks them
+    (nvcc cross-compiles sm_100a without a GPU; the oracle is plain gcc)."""
+    import subprocess
+    so = os.path.join(REPO, "paper_1401_0248_b200", "libtwofold_b200.so")
+    tfo = os.path.join(REPO, "oracle", "build", "libtfo.so")
+    if not os.path.exists(tfo):
+        subprocess.run(["make", "-s", "-C", os.path.join(REPO, "oracle")], check=True)
+    if not os.path.exists(so):
+        subprocess.run(["make", "-s", "-j4", "-C", os.path.join(REPO, "paper_1401_0248_b200", "csrc")], check=True)
 
 
 @pytest.fixture(scope="session")
