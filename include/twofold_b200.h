@@ -79,6 +79,8 @@ int tf_version(void);
 const char* tf_strerror(int code);
 /* Text of the last CUDA error seen by this thread ("" if none). */
 const char* tf_last_cuda_error(void);
+/* Number of kernels this library has launched in this process (all threads). */
+uint64_t tf_launch_count(void);
 
 /* Device strict-rounding canary: runs the kernels' own EFT and dot-step code on
  * runtime operands — fast_two_sum(1, 2^-53) must return (1, 2^-53) in f64 and

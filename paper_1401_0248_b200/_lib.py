@@ -36,6 +36,7 @@ def _bind(L):
         "tf_version": ([], i32),
         "tf_strerror": ([i32], ctypes.c_char_p),
         "tf_last_cuda_error": ([], ctypes.c_char_p),
+        "tf_launch_count": ([], ctypes.c_uint64),
         "tf_canary": ([], i32),
         "tf_leaf_log2": ([i32, i64], i32),
         "tf_set_leaf_split": ([i32], i32),

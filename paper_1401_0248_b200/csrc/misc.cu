@@ -18,6 +18,11 @@ namespace tfb {
 
 static thread_local char g_cuda_err[256] = {0};
 
+std::atomic<uint64_t>& launch_counter() {
+  static std::atomic<uint64_t> c{0};
+  return c;
+}
+
 void set_cuda_error(cudaError_t e) {
   std::snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e),
                 cudaGetErrorString(e));
@@ -277,6 +282,8 @@ const char* tf_strerror(int code) {
 }
 
 const char* tf_last_cuda_error(void) { return g_cuda_err; }
+
+uint64_t tf_launch_count(void) { return launch_counter().load(std::memory_order_relaxed); }
 
 int tf_canary(void) {
   const double in[8] = {1.0, 0x1p-53, 0x1p-24, 1.0 + 0x1p-30, -(1.0 + 0x1p-29),

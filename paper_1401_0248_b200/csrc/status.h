@@ -2,6 +2,9 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
+#include <cstdint>
+
 #include "twofold_b200.h"
 
 namespace tfb {
@@ -14,7 +17,12 @@ inline int record_cuda_error() {
   return TF_ECUDA;
 }
 
+// Process-wide count of kernels this library launched (tf_launch_count()).
+std::atomic<uint64_t>& launch_counter();
+
+// Called right after every kernel launch.
 inline int check_launch() {
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_cuda_error(e);
