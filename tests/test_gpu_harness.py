@@ -78,3 +78,43 @@ def test_table1_orderings(H):
             assert cell[(name, p, "large")] >= 0.9 * cell[("sum", p, "large")], (name, p)
         for name in ("dottf", "dott", "dotk"):
             assert cell[(name, p, "large")] >= 0.9 * cell[("dot", p, "large")], (name, p)
+
+
+def test_error_sign_fidelity_grid(H):
+    """test_accuracy.py:54-66 on the grid flavor: whenever the value deviation is
+    resolvable, the error channel has the sign of (exact - value)."""
+    import math
+    import paper_1401_0248_b200 as tfb
+    checked = 0
+    for seed in range(1, 8):
+        for sym in (False, True):
+            data = tfb.lcg_fill("mmix", 1_000_000, seed, torch.float32, sym)
+            ref = tfb.exact_sum(data)
+            r = tfb.sum_twofold_fast(data)
+            rel_value = tfb.relative_error(float(np.float64(r.value)), ref)
+            if abs(rel_value) > 10 * 2.0 ** -24:
+                assert math.copysign(1, float(r.error)) == math.copysign(1, float(ref) - float(r.value))
+                checked += 1
+    # the tree sum is far more accurate than sequential, so few cases resolve;
+    # also check the sign on cancellation-heavy cfg3-style data where it always does
+    x = tfb.philox_fill("illcond", 1 << 22, seed=2, total=1 << 22)
+    ref = tfb.exact_sum(x)
+    r = tfb.sum_twofold_rigorous(x)
+    assert math.copysign(1, float(r.error)) == math.copysign(1, float(ref.hi) - float(r.value))
+
+
+def test_eft_ulp_bound_nonfinite_and_exact_permutation(cuda):
+    """test_eft.py:74-103 (|y| <= ulp(x), non-finite propagation) on the device EFTs,
+    and test_expansion.py:88-99 (permutation invariance) on the GPU exact oracle."""
+    import math
+    import paper_1401_0248_b200 as tfb
+    rng = np.random.default_rng(9)
+    a = rng.standard_normal(50_000) * 2.0 ** rng.integers(-300, 300, 50_000)
+    b = rng.standard_normal(50_000) * 2.0 ** rng.integers(-300, 300, 50_000)
+    x, y = tfb.two_sum(a, b)
+    nz = x != 0
+    assert np.all(np.abs(y[nz]) <= np.array([math.ulp(v) for v in x[nz]]))
+    xi, _ = tfb.two_sum(np.array([math.inf, 1e308]), np.array([1.0, 1e308]))
+    assert math.isinf(xi[0]) and not math.isfinite(xi[1])
+    v = rng.uniform(-1e6, 1e6, 30_001)
+    assert tfb.exact_sum(v).fraction() == tfb.exact_sum(rng.permutation(v)).fraction()
