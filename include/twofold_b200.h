@@ -251,6 +251,26 @@ int tf_fill_rows_scaled(int dtype, uint64_t seed, uint64_t stream_id,
                         int64_t cols, int64_t ld, double lo, double hi,
                         void* out, void* stream);
 
+/* Host-buffer engine — the reference's blocking call on HOST memory as one
+ * native call: run_flavor(method, Flavor("cuda"), data, b) (kernels.py:591-640)
+ * where data/b are numpy arrays.  An engine owns a stream, two staging slots
+ * (pinned + device, chunk_bytes per operand; 0 = 16 MiB, min 1 MiB), grown-on-
+ * demand scratch and a `threads`-wide memcpy pool (0 = min(8, cores/2)); it
+ * allocates at creation and when the scratch grows — the one exception to "no
+ * function allocates".  engine: out, an opaque handle. */
+int tf_host_engine_create(int device, int threads, size_t chunk_bytes, void** engine);
+int tf_host_engine_destroy(void* engine);
+int tf_host_engine_threads(const void* engine);
+
+/* (value, error) of x[, y] (n elements each) into out_pair_host (2 accumulator
+ * elements, host memory); blocks until done.  Pageable inputs go through the
+ * pinned slots (the pool copies chunk c+1 while chunk c is on the DMA engine
+ * and its leaves reduce); page-locked inputs DMA directly; device pointers
+ * reduce in place.  Leaf-aligned chunks: bit-identical to tf_reduce.  Calls on
+ * one engine are serialised. */
+int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const void* hy, int64_t n,
+                   int leaf_log2, void* out_pair_host);
+
 #ifdef __cplusplus
 }
 #endif

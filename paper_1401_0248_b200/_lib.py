@@ -62,6 +62,10 @@ def _bind(L):
         "tf_fill_host": ([i32, i32, u64, u64, u64, i64, dbl, dbl, dbl, i64, vp, i32], i32),
         "tf_lcg_fill": ([i32, i32, u64, i32, i64, i64, vp, vp], i32),
         "tf_fill_rows_scaled": ([i32, u64, u64, u64, i64, i64, i64, i64, dbl, dbl, vp, vp], i32),
+        "tf_host_engine_create": ([i32, i32, sz, ctypes.POINTER(vp)], i32),
+        "tf_host_engine_destroy": ([vp], i32),
+        "tf_host_engine_threads": ([vp], i32),
+        "tf_host_reduce": ([vp, i32, i32, vp, vp, i64, i32, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -114,3 +118,36 @@ def ensure_canary(device_index: int) -> None:
             "error tracking")
     check(rc, "tf_canary")
     _canary_ok.add(device_index)
+
+
+_engines: dict = {}
+_default_engines: dict = {}
+
+
+def host_engine(device_index: int, chunk_bytes: int | None = None, threads: int | None = None):
+    """The host-buffer engine (tf_host_engine_create) for one device and
+    configuration, created once.  Defaults: TFB_HOST_THREADS (0 = auto) and
+    TFB_HOST_CHUNK_MB (0 = 16 MiB per operand per slot)."""
+    if chunk_bytes is None and threads is None:
+        eng = _default_engines.get(device_index)
+        if eng is not None:
+            return eng
+        eng = host_engine(device_index, int(os.environ.get("TFB_HOST_CHUNK_MB", "0")) << 20,
+                          int(os.environ.get("TFB_HOST_THREADS", "0")))
+        _default_engines[device_index] = eng
+        return eng
+    if threads is None:
+        threads = int(os.environ.get("TFB_HOST_THREADS", "0"))
+    if chunk_bytes is None:
+        chunk_bytes = int(os.environ.get("TFB_HOST_CHUNK_MB", "0")) << 20
+    key = (device_index, chunk_bytes, threads)
+    eng = _engines.get(key)
+    if eng is None:
+        with _lock:
+            eng = _engines.get(key)
+            if eng is None:
+                eng = ctypes.c_void_p()
+                check(lib().tf_host_engine_create(device_index, threads, chunk_bytes, ctypes.byref(eng)),
+                      "tf_host_engine_create")
+                _engines[key] = eng
+    return eng

@@ -24,6 +24,7 @@ fallback: without the CUDA library or a GPU every compute call raises.
 from __future__ import annotations
 
 import ctypes
+import functools
 import threading
 from dataclasses import dataclass
 from enum import Enum
@@ -263,11 +264,16 @@ _scratch = _Scratch()
 
 
 def workspace_size(method: Method, dtype: torch.dtype, rows: int, cols: int, leaf_log2: int = 0):
+    """(partials bytes, counters, leaves per row) — a pure function, cached."""
+    return _workspace_size(_METHOD_ID[method], _dtype_code(dtype), rows, cols, leaf_log2)
+
+
+@functools.lru_cache(maxsize=4096)
+def _workspace_size(mid: int, dcode: int, rows: int, cols: int, leaf_log2: int):
     pb = ctypes.c_size_t(0)
     cnt = ctypes.c_int64(0)
     leaves = ctypes.c_int64(0)
-    check(lib().tf_workspace_size(_METHOD_ID[method], _dtype_code(dtype), rows, cols, leaf_log2,
-                                  pb, cnt, leaves), "tf_workspace_size")
+    check(lib().tf_workspace_size(mid, dcode, rows, cols, leaf_log2, pb, cnt, leaves), "tf_workspace_size")
     return pb.value, cnt.value, leaves.value
 
 
@@ -318,71 +324,30 @@ def merge_pairs(method: Method, pairs: torch.Tensor, out: torch.Tensor | None = 
         return out
 
 
-_CHUNK_BYTES = 64 << 20  # per operand, per staging buffer
-
-
-class _CopyStreams:
-    def __init__(self):
-        self._s: dict[int, torch.cuda.Stream] = {}
-        self._lock = threading.Lock()
-
-    def get(self, dev: torch.device) -> torch.cuda.Stream:
-        with self._lock:
-            s = self._s.get(dev.index)
-            if s is None:
-                s = torch.cuda.Stream(device=dev)
-                self._s[dev.index] = s
-            return s
-
-
-_copy_streams = _CopyStreams()
-
-
-def _reduce_grid_host(method: Method, x: torch.Tensor, y: torch.Tensor | None, dev: torch.device,
-                      leaf_log2: int = 0, track_product: bool = False) -> torch.Tensor:
-    """Grid flavor for host inputs: leaf-aligned chunks are copied H2D on a side
-    stream (double-buffered) while the previous chunk's leaves reduce; the
-    final tree runs over all leaf pairs — bit-identical to the device path."""
-    n = x.numel()
-    lg = leaf_log2 or leaf_log2_for(x.dtype, n)
-    L = 1 << lg
-    P = -(-n // L)
-    item = x.element_size()
-    chunk_leaves = max(1, _CHUNK_BYTES // (L * item))
-    if P <= chunk_leaves:
-        return _reduce_grid(method, _on_device(x, dev), _on_device(y, dev), lg, track_product=track_product)
+def _host_pair(method: Method, x: torch.Tensor, y: torch.Tensor | None, dev: torch.device,
+               leaf_log2: int = 0, track_product: bool = False, engine=None) -> np.ndarray:
+    """Grid flavor on HOST tensors through the native host-buffer engine
+    (tf_host_reduce, csrc/host.cu): pinned staging, leaf-aligned chunks whose
+    copies overlap the leaf kernels, blocking; bit-identical to the device path.
+    Returns the raw (value, error) pair as a numpy array."""
     _lib.ensure_canary(dev.index)
-    acc = _acc_dtype(method, x.dtype)
-    pair_bytes = 2 * torch.empty(0, dtype=acc).element_size()
-    compute = torch.cuda.current_stream(dev)
-    copy = _copy_streams.get(dev)
-    chunk = chunk_leaves * L
-    xs = [torch.empty(chunk, dtype=x.dtype, device=dev) for _ in range(2)]
-    ys = [torch.empty(chunk, dtype=x.dtype, device=dev) for _ in range(2)] if y is not None else None
-    partials = torch.empty(P * pair_bytes, dtype=torch.uint8, device=dev)
-    ready = [torch.cuda.Event() for _ in range(2)]
-    free = [torch.cuda.Event() for _ in range(2)]
-    nchunks = -(-n // chunk)
-    for c in range(nchunks):
-        b = c & 1
-        lo = c * chunk
-        hi = min(n, lo + chunk)
-        with torch.cuda.stream(copy):
-            copy.wait_event(free[b])
-            xs[b][: hi - lo].copy_(x[lo:hi], non_blocking=True)
-            if y is not None:
-                ys[b][: hi - lo].copy_(y[lo:hi], non_blocking=True)
-            ready[b].record(copy)
-        compute.wait_event(ready[b])
-        _reduce_leaves(method, xs[b][: hi - lo], None if y is None else ys[b][: hi - lo], lg,
-                       partials.data_ptr() + c * chunk_leaves * pair_bytes, compute.cuda_stream, track_product)
-        free[b].record(compute)
-    for t in xs + (ys or []):
-        t.record_stream(copy)
-    out = torch.empty(2, dtype=acc, device=dev)
-    check(lib().tf_merge_tree(_METHOD_ID[method], _dtype_code(x.dtype), partials.data_ptr(), P,
-                              out.data_ptr(), compute.cuda_stream), "tf_merge_tree")
-    return out
+    x = x.contiguous()
+    y = None if y is None else y.contiguous()
+    pair = np.empty(2, dtype=_np_type(_acc_dtype(method, x.dtype)))
+    eng = engine if engine is not None else _lib.host_engine(dev.index)
+    check(lib().tf_host_reduce(eng, _mid(method, track_product, y is not None), _dtype_code(x.dtype),
+                               x.data_ptr(), None if y is None else y.data_ptr(), x.numel(), leaf_log2,
+                               pair.ctypes.data), "tf_host_reduce")
+    return pair
+
+
+def _reduce_host(method: Method, x: torch.Tensor, y: torch.Tensor | None, dev: torch.device,
+                 leaf_log2: int = 0, out: torch.Tensor | None = None, track_product: bool = False) -> torch.Tensor:
+    """_host_pair, delivered as a 2-element device tensor (reduce()'s result form)."""
+    pair = torch.from_numpy(_host_pair(method, x, y, dev, leaf_log2, track_product))
+    if out is None:
+        return pair.to(dev)
+    return out.copy_(pair)
 
 
 def _reduce_seq(method: Method, x, y, dev, track_product: bool = False) -> torch.Tensor:
@@ -414,9 +379,9 @@ def reduce(method: Method, data, b=None, *, flavor: Flavor = _CUDA, leaf_log2: i
     dev = _device_for(x)
     with torch.cuda.device(dev):  # the C library launches on the current device
         if flavor.kind == "cuda":
-            if x.is_cuda:
-                return _reduce_grid(method, _on_device(x, dev), _on_device(y, dev), leaf_log2, out, track_product)
-            return _reduce_grid_host(method, x, y, dev, leaf_log2, track_product)
+            if _all_host(x, y):
+                return _reduce_host(method, x, y, dev, leaf_log2, out, track_product)
+            return _reduce_grid(method, _on_device(x, dev), _on_device(y, dev), leaf_log2, out, track_product)
         xd, yd = _on_device(x, dev), _on_device(y, dev)
         if flavor.kind == "seq":
             return _reduce_seq(method, xd, yd, dev, track_product)
@@ -424,8 +389,12 @@ def reduce(method: Method, data, b=None, *, flavor: Flavor = _CUDA, leaf_log2: i
         return _reduce_lanes(method, xd, yd, k, dev, track_product)
 
 
-def _finish(method: Method, pair: torch.Tensor, dtype: torch.dtype, n: int) -> SumResult:
-    v, e = pair.cpu().tolist()
+def _all_host(x: torch.Tensor, y: torch.Tensor | None) -> bool:
+    return not x.is_cuda and (y is None or not y.is_cuda)
+
+
+def _finish(method: Method, pair, dtype: torch.dtype, n: int) -> SumResult:
+    v, e = (pair.cpu() if torch.is_tensor(pair) else pair).tolist()
     t = np.float64 if method is Method.WIDE else _np_type(dtype)
     if method in _TWOFOLD_METHODS:
         return SumResult(Twofold(t(v), t(e)), n)
@@ -441,14 +410,63 @@ def run_flavor(method: Method, flavor: Flavor, data, b=None, *, track_product: b
     ("cuda", "unroll", "vec") associate differently from "seq" and are not
     bitwise reproductions of it; they satisfy the same accuracy contracts.
     """
+    if flavor.kind == "cuda" and type(data) is np.ndarray and (b is None or type(b) is np.ndarray):
+        return _run_numpy(method, data, b, track_product)
     x, y = _check_input(data, b)
     n = x.numel()
     if method is Method.WIDE and x.dtype != torch.float32:
         raise TypeError("wide accumulation is defined for float32 data only")
     if method not in _METHOD_ID:
         raise ValueError(f"unknown method {method!r}")
-    pair = reduce(method, x, y, flavor=flavor, track_product=track_product)
+    if flavor.kind == "cuda" and _all_host(x, y):  # host arrays: one blocking native call
+        _mid(method, track_product, y is not None)
+        pair = _host_pair(method, x, y, _device_for(x), track_product=track_product)
+    else:
+        pair = reduce(method, x, y, flavor=flavor, track_product=track_product)
     return _finish(method, pair, x.dtype, n)
+
+
+_NP_CODE = {np.dtype(np.float32): _lib.TF_F32, np.dtype(np.float64): _lib.TF_F64}
+
+
+def _run_numpy(method: Method, a: np.ndarray, b: np.ndarray | None, track_product: bool) -> SumResult:
+    """run_flavor(method, "cuda", a[, b]) for numpy arrays: the same checks and
+    result as the general path, minus the torch round trip — host pointers go
+    straight to the native host-buffer engine (tf_host_reduce)."""
+    code = _NP_CODE.get(a.dtype)
+    if code is None:
+        raise TypeError(f"unsupported dtype {a.dtype}; use float32/float64")
+    if a.ndim != 1:
+        raise ValueError(f"expected a 1-D array, got shape {a.shape}")
+    if b is not None:
+        if _NP_CODE.get(b.dtype) is None:
+            raise TypeError(f"unsupported dtype {b.dtype}; use float32/float64")
+        if b.ndim != 1:
+            raise ValueError(f"expected a 1-D array, got shape {b.shape}")
+        if b.dtype != a.dtype:
+            raise TypeError("dot operands must share a dtype")
+        if b.shape != a.shape:
+            raise ValueError("dot operands must have equal length")
+    if method is Method.WIDE and code != _lib.TF_F32:
+        raise TypeError("wide accumulation is defined for float32 data only")
+    if method not in _METHOD_ID:
+        raise ValueError(f"unknown method {method!r}")
+    mid = _mid(method, track_product, b is not None)
+    if not a.flags.c_contiguous:
+        a = np.ascontiguousarray(a)
+    if b is not None and not b.flags.c_contiguous:
+        b = np.ascontiguousarray(b)
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device available: the twofold B200 library has no CPU path")
+    dev = torch.cuda.current_device()
+    _lib.ensure_canary(dev)
+    pair = np.empty(2, dtype=np.float64 if method is Method.WIDE else a.dtype)
+    check(lib().tf_host_reduce(_lib.host_engine(dev), mid, code, a.ctypes.data,
+                               None if b is None else b.ctypes.data, a.shape[0], 0, pair.ctypes.data),
+          "tf_host_reduce")
+    if method in _TWOFOLD_METHODS:
+        return SumResult(Twofold(pair[0], pair[1]), a.shape[0])
+    return SumResult(Twofold(pair[0], pair.dtype.type(0)), a.shape[0])
 
 
 def raw_sum_kernel(method: Method, flavor: Flavor, dtype):

@@ -1,0 +1,365 @@
+// host.cu — host-buffer engine: the reference's blocking call shape
+// (run_flavor(method, Flavor("cuda"), data, b) -> pair, kernels.py:591-640)
+// on host memory, as one native call.
+//
+// An engine owns, per device: a non-blocking stream, two staging slots (pinned
+// host + device, `chunk` bytes per operand each), grow-on-demand leaf partials
+// and retire counters, a pinned result pair, and a small memcpy thread pool.
+//
+// tf_host_reduce(engine, method, dtype, hx, hy, n, leaf_log2, out_pair_host):
+//   * n fits one chunk: stage -> H2D per operand -> tf_reduce (fused; its
+//     last CTA stores the pair into mapped pinned memory) -> stream sync;
+//   * larger: leaf-aligned chunks; while the DMA engine moves chunk c and the
+//     GPU reduces its leaves (tf_reduce_leaves into partials + c*chunk_leaves),
+//     the pool copies chunk c+1 into the other pinned slot; tf_merge_tree
+//     closes the tree.  Chunks are whole leaves, so the partials and the tree
+//     are exactly those of tf_reduce on the whole array: bit-identical.
+//   * page-locked inputs (cudaHostAlloc / cudaHostRegister) skip the staging
+//     copy and DMA straight from the caller's memory; device pointers skip the
+//     copies altogether.
+//   * pageable staging is pipelined in 2 MiB pieces (the DMA of piece i
+//     overlaps the pool's copy of piece i+1).
+// Calls on one engine are serialised by its mutex; the call blocks until the
+// pair is in out_pair_host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "status.h"
+
+namespace tfb {
+namespace {
+
+// Fixed-size pool: copy(dst, src, bytes) splits the range into one piece per
+// worker (plus the calling thread) and returns when all pieces are done.
+// Workers spin for up to kSpinUs after a job (the next piece of a pipelined
+// stage usually follows within microseconds) and then sleep on a condvar.
+class CopyPool {
+ public:
+  static constexpr int kSpinUs = 200;
+  explicit CopyPool(int workers) {
+    for (int i = 0; i < workers; ++i) workers_.emplace_back([this, i] { run(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_.store(true);
+      gen_.fetch_add(1);
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  int threads() const { return static_cast<int>(workers_.size()) + 1; }
+
+  void copy(void* dst, const void* src, size_t bytes) {
+    const int parts = threads();
+    if (bytes < (size_t(256) << 10) || parts == 1) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    dst_ = static_cast<char*>(dst);
+    src_ = static_cast<const char*>(src);
+    bytes_ = bytes;
+    pending_.store(parts - 1, std::memory_order_relaxed);
+    {
+      std::lock_guard<std::mutex> g(m_);
+      gen_.fetch_add(1, std::memory_order_release);
+    }
+    cv_.notify_all();
+    piece(parts - 1);
+    while (pending_.load(std::memory_order_acquire) != 0) pause();
+  }
+
+ private:
+  static void pause() {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  void piece(int i) {
+    const int parts = threads();
+    const size_t per = ((bytes_ / parts) + 4095) & ~size_t(4095);
+    const size_t lo = std::min(bytes_, per * i);
+    const size_t hi = i == parts - 1 ? bytes_ : std::min(bytes_, per * (i + 1));
+    if (hi > lo) std::memcpy(dst_ + lo, src_ + lo, hi - lo);
+  }
+  void run(int i) {
+    uint64_t seen = 0;
+    for (;;) {
+      auto t0 = std::chrono::steady_clock::now();
+      int k = 0;
+      while (gen_.load(std::memory_order_acquire) == seen) {
+        pause();
+        if ((++k & 63) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(kSpinUs)) {
+          std::unique_lock<std::mutex> lk(m_);
+          cv_.wait(lk, [&] { return gen_.load(std::memory_order_acquire) != seen; });
+          break;
+        }
+      }
+      seen = gen_.load(std::memory_order_acquire);
+      if (stop_.load()) return;
+      piece(i);
+      pending_.fetch_sub(1, std::memory_order_release);
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_;
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> pending_{0};
+  std::atomic<bool> stop_{false};
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+enum class Mem { kPageable, kPinned, kDevice };
+
+Mem classify(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return Mem::kPageable;
+  }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return Mem::kDevice;
+  if (a.type == cudaMemoryTypeHost) return Mem::kPinned;
+  return Mem::kPageable;
+}
+
+}  // namespace
+
+struct HostEngine {
+  int device = 0;
+  size_t chunk = 0;  // bytes per operand per slot
+  cudaStream_t stream = nullptr;
+  char* pin[2] = {nullptr, nullptr};  // [x | y] per slot
+  char* dev[2] = {nullptr, nullptr};
+  cudaEvent_t h2d_done[2] = {nullptr, nullptr};
+  void* pair_pin = nullptr;  // mapped pinned: the last kernel stores the pair straight into it
+  void* partials = nullptr;
+  size_t partials_bytes = 0;
+  void* counters = nullptr;
+  int64_t counters_len = 0;
+  CopyPool* pool = nullptr;
+  std::mutex mu;
+};
+
+namespace {
+
+int cu(cudaError_t e) {
+  if (e == cudaSuccess) return TF_OK;
+  set_cuda_error(e);
+  cudaGetLastError();
+  return TF_ECUDA;
+}
+
+void release(HostEngine* g) {
+  for (int b = 0; b < 2; ++b) {
+    if (g->pin[b]) cudaFreeHost(g->pin[b]);
+    if (g->dev[b]) cudaFree(g->dev[b]);
+    if (g->h2d_done[b]) cudaEventDestroy(g->h2d_done[b]);
+  }
+  if (g->pair_pin) cudaFreeHost(g->pair_pin);
+  if (g->partials) cudaFree(g->partials);
+  if (g->counters) cudaFree(g->counters);
+  if (g->stream) cudaStreamDestroy(g->stream);
+  delete g->pool;
+  delete g;
+}
+
+// Grow the scratch to at least (pb bytes, cnt counters); counters are zeroed.
+int ensure_scratch(HostEngine* g, size_t pb, int64_t cnt) {
+  int rc;
+  if (pb > g->partials_bytes) {
+    if ((rc = cu(cudaStreamSynchronize(g->stream)))) return rc;
+    if (g->partials) cudaFree(g->partials);
+    g->partials = nullptr;
+    g->partials_bytes = 0;
+    if ((rc = cu(cudaMalloc(&g->partials, pb)))) return rc;
+    g->partials_bytes = pb;
+  }
+  if (cnt > g->counters_len) {
+    if ((rc = cu(cudaStreamSynchronize(g->stream)))) return rc;
+    if (g->counters) cudaFree(g->counters);
+    g->counters = nullptr;
+    g->counters_len = 0;
+    if ((rc = cu(cudaMalloc(&g->counters, sizeof(unsigned) * cnt)))) return rc;
+    if ((rc = cu(cudaMemsetAsync(g->counters, 0, sizeof(unsigned) * cnt, g->stream)))) return rc;
+    g->counters_len = cnt;
+  }
+  return TF_OK;
+}
+
+constexpr size_t kPiece = size_t(2) << 20;
+
+// Stage `bytes` of operand k (0 = x, 1 = y) from host `src` into device slot b.
+int stage(HostEngine* g, int b, int k, const char* src, size_t bytes, Mem kind, bool wait_slot) {
+  char* d = g->dev[b] + k * g->chunk;
+  if (kind == Mem::kPinned) return cu(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, g->stream));
+  if (wait_slot) {
+    int rc = cu(cudaEventSynchronize(g->h2d_done[b]));  // the slot's previous DMA has drained
+    if (rc) return rc;
+  }
+  // Pieces: the DMA of piece i overlaps the host copy of piece i+1.
+  char* p = g->pin[b] + k * g->chunk;
+  for (size_t off = 0; off < bytes; off += kPiece) {
+    const size_t m = std::min(kPiece, bytes - off);
+    g->pool->copy(p + off, src + off, m);
+    int rc = cu(cudaMemcpyAsync(d + off, p + off, m, cudaMemcpyHostToDevice, g->stream));
+    if (rc) return rc;
+  }
+  return TF_OK;
+}
+
+}  // namespace
+}  // namespace tfb
+
+using tfb::HostEngine;
+
+extern "C" {
+
+int tf_host_engine_create(int device, int threads, size_t chunk_bytes, void** engine) {
+  if (!engine) return TF_EINVAL_ARG;
+  *engine = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess) return tfb::record_cuda_error();
+  if (device < 0 || device >= ndev) return TF_EINVAL_ARG;
+  if (chunk_bytes == 0) chunk_bytes = size_t(16) << 20;
+  // A chunk must hold at least one maximal leaf (2^16 f64 = 512 KiB).
+  chunk_bytes = std::max(chunk_bytes, size_t(1) << 20);
+  chunk_bytes = (chunk_bytes + 4095) & ~size_t(4095);
+  if (threads <= 0) {
+    const unsigned hw = std::thread::hardware_concurrency();
+    threads = static_cast<int>(std::min(8u, std::max(1u, hw / 2)));
+  }
+  tfb::DeviceGuard guard(device);
+  auto* g = new HostEngine();
+  g->device = device;
+  g->chunk = chunk_bytes;
+  int rc = TF_OK;
+  auto step = [&](cudaError_t e) {
+    if (rc == TF_OK) rc = tfb::cu(e);
+  };
+  step(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+  for (int b = 0; b < 2 && rc == TF_OK; ++b) {
+    step(cudaHostAlloc(reinterpret_cast<void**>(&g->pin[b]), 2 * chunk_bytes, cudaHostAllocDefault));
+    step(cudaMalloc(reinterpret_cast<void**>(&g->dev[b]), 2 * chunk_bytes));
+    step(cudaEventCreateWithFlags(&g->h2d_done[b], cudaEventDisableTiming));
+  }
+  step(cudaHostAlloc(&g->pair_pin, 16, cudaHostAllocMapped));
+  if (rc != TF_OK) {
+    tfb::release(g);
+    return rc;
+  }
+  g->pool = new tfb::CopyPool(threads - 1);
+  *engine = g;
+  return TF_OK;
+}
+
+int tf_host_engine_destroy(void* engine) {
+  if (!engine) return TF_OK;
+  auto* g = static_cast<HostEngine*>(engine);
+  {
+    tfb::DeviceGuard guard(g->device);
+    std::lock_guard<std::mutex> lk(g->mu);
+    cudaStreamSynchronize(g->stream);
+  }
+  tfb::DeviceGuard guard(g->device);
+  tfb::release(g);
+  return TF_OK;
+}
+
+int tf_host_engine_threads(const void* engine) {
+  return engine ? static_cast<const HostEngine*>(engine)->pool->threads() : 0;
+}
+
+int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const void* hy, int64_t n,
+                   int leaf_log2, void* out_pair_host) {
+  if (!engine || !out_pair_host) return TF_EINVAL_ARG;
+  if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
+  if (n < 0) return TF_EINVAL_SHAPE;
+  if (n > 0 && !hx) return TF_EINVAL_ARG;
+  auto* g = static_cast<HostEngine*>(engine);
+  std::lock_guard<std::mutex> lk(g->mu);
+  tfb::DeviceGuard guard(g->device);
+  const int base = method & ~TF_TRACK_PRODUCT;
+  const size_t pair_bytes = (base == TF_WIDE ? 8 : (dtype == TF_F64 ? 8 : 4)) * 2;
+  const size_t item = dtype == TF_F64 ? 8 : 4;
+  const bool dot = hy != nullptr;
+
+  size_t pb = 0;
+  int64_t cnt = 0, leaves = 0;
+  int rc = tf_workspace_size(method, dtype, 1, n, leaf_log2, &pb, &cnt, &leaves);
+  if (rc) return rc;
+  const int lg = leaf_log2 ? leaf_log2 : tf_leaf_log2(dtype, n);
+  if ((rc = tfb::ensure_scratch(g, std::max<size_t>(pb, pair_bytes), std::max<int64_t>(cnt, 1)))) return rc;
+
+  const tfb::Mem kx = n > 0 ? tfb::classify(hx) : tfb::Mem::kPageable;
+  const tfb::Mem ky = dot && n > 0 ? tfb::classify(hy) : kx;
+  if (kx == tfb::Mem::kDevice && ky == tfb::Mem::kDevice) {  // already resident: plain tf_reduce
+    rc = tf_reduce(method, dtype, hx, hy, n, leaf_log2, g->pair_pin, g->partials, g->partials_bytes,
+                   g->counters, g->counters_len, g->stream);
+  } else if (kx == tfb::Mem::kDevice || ky == tfb::Mem::kDevice) {
+    return TF_EINVAL_ARG;  // mixed host/device operands
+  } else {
+    const int64_t L = int64_t(1) << lg;
+    const int64_t chunk_leaves = std::max<int64_t>(1, static_cast<int64_t>(g->chunk / (L * item)));
+    const int64_t chunk_elems = chunk_leaves * L;
+    const auto* cx = static_cast<const char*>(hx);
+    const auto* cy = static_cast<const char*>(hy);
+    if (n <= chunk_elems) {
+      const size_t bytes = n * item;
+      if (n > 0) {
+        if ((rc = tfb::stage(g, 0, 0, cx, bytes, kx, true))) return rc;
+        if (dot && (rc = tfb::stage(g, 0, 1, cy, bytes, ky, true))) return rc;
+        if ((rc = tfb::cu(cudaEventRecord(g->h2d_done[0], g->stream)))) return rc;
+      }
+      rc = tf_reduce(method, dtype, g->dev[0], dot ? g->dev[0] + g->chunk : nullptr, n, lg, g->pair_pin,
+                     g->partials, g->partials_bytes, g->counters, g->counters_len, g->stream);
+    } else {
+      const int64_t nchunks = (n + chunk_elems - 1) / chunk_elems;
+      for (int64_t c = 0; c < nchunks && rc == TF_OK; ++c) {
+        const int b = static_cast<int>(c & 1);
+        const int64_t lo = c * chunk_elems;
+        const int64_t m = std::min(n, lo + chunk_elems) - lo;
+        const size_t bytes = m * item;
+        if ((rc = tfb::stage(g, b, 0, cx + lo * item, bytes, kx, c >= 2))) break;
+        if (dot && (rc = tfb::stage(g, b, 1, cy + lo * item, bytes, ky, c >= 2))) break;
+        if ((rc = tfb::cu(cudaEventRecord(g->h2d_done[b], g->stream)))) break;
+        rc = tf_reduce_leaves(method, dtype, g->dev[b], dot ? g->dev[b] + g->chunk : nullptr, m, lg,
+                              static_cast<char*>(g->partials) + c * chunk_leaves * pair_bytes, g->stream);
+      }
+      if (rc == TF_OK)
+        rc = tf_merge_tree(method, dtype, g->partials, leaves, g->pair_pin, g->stream);
+    }
+  }
+  if (rc) {
+    cudaStreamSynchronize(g->stream);
+    return rc;
+  }
+  if ((rc = tfb::cu(cudaStreamSynchronize(g->stream)))) return rc;
+  std::memcpy(out_pair_host, g->pair_pin, pair_bytes);
+  return TF_OK;
+}
+
+}  // extern "C"

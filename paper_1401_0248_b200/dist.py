@@ -50,13 +50,15 @@ def shard_range(n: int, rank: int, world: int, leaf_log2: int) -> tuple[int, int
 
 
 def _default_local(method: Method, x: torch.Tensor, y, leaf_log2: int, track_product: bool = False) -> torch.Tensor:
-    from .api import _device_for, _on_device, _reduce_grid, _reduce_grid_host
-    if x.is_cuda:
-        with torch.cuda.device(x.device):
-            return _reduce_grid(method, x.contiguous(), _on_device(y, x.device), leaf_log2,
-                                track_product=track_product)
-    # host shard: leaf-aligned chunks streamed H2D, overlapped with the leaf kernels
-    return _reduce_grid_host(method, x, y, _device_for(x), leaf_log2, track_product)
+    from .api import _all_host, _device_for, _on_device, _reduce_grid, _reduce_host
+    dev = _device_for(x)
+    with torch.cuda.device(dev):
+        if _all_host(x, y):
+            # host shard: the native host-buffer engine (pinned staging, chunked H2D
+            # overlapped with the leaf kernels)
+            return _reduce_host(method, x, y, dev, leaf_log2, track_product=track_product)
+        return _reduce_grid(method, _on_device(x, dev), _on_device(y, dev), leaf_log2,
+                            track_product=track_product)
 
 
 def _default_merge(method: Method, pairs: torch.Tensor) -> torch.Tensor:

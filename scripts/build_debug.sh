@@ -3,7 +3,7 @@
 set -e
 cd "$(dirname "$0")/../paper_1401_0248_b200/csrc"
 mkdir -p ../variants build_debug
-for f in reduce misc exact; do
+for f in reduce misc exact host; do
   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -fmad=false -ftz=false -prec-div=true \
     -prec-sqrt=true -lineinfo -Xcompiler -fPIC -I../../include -DTFB_DEBUG=1 -c $f.cu -o build_debug/$f.o &
 done

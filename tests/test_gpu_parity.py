@@ -187,9 +187,12 @@ def test_rows_strided_leading_dimension(tfb, oracle, cuda):
         _same(got[r], (ev[r], ee[r]), r)
 
 
-def test_streamed_host_path_equals_device_path(tfb, oracle, cuda, monkeypatch):
-    from paper_1401_0248_b200 import api
-    monkeypatch.setattr(api, "_CHUNK_BYTES", 1 << 16)  # force many chunks
+def test_streamed_host_path_equals_device_path(tfb, oracle, cuda):
+    """Host-buffer engine (tf_host_reduce): 1 MiB chunks force 17 chunks of 16
+    leaves; pageable and pinned inputs, sums and dots, equal the emulator."""
+    from paper_1401_0248_b200 import _lib, api
+    eng = _lib.host_engine(0, chunk_bytes=1 << 20, threads=3)
+    dev = torch.device("cuda", 0)
     n = (1 << 21) + 5
     xh = oracle.lcg_fill("mmix", n, 21, np.float64, True)
     yh = oracle.lcg_fill("nr", n, 22, np.float64, True)
@@ -199,10 +202,24 @@ def test_streamed_host_path_equals_device_path(tfb, oracle, cuda, monkeypatch):
             xt, yt = xt.pin_memory(), yt.pin_memory()
         for m in (0, 2, 3, 4):
             meth = list(tfb.Method)[m]
-            got = tfb.reduce(meth, xt, yt).cpu().numpy()
+            got = api._host_pair(meth, xt, yt, dev, engine=eng)
             _same(got, oracle.emulate(m, xh, yh), (m, pinned))
-    r = tfb.dot_twofold_fast(xh, yh)  # numpy inputs through the public wrapper
+            got = api._host_pair(meth, xt, None, dev, engine=eng)
+            _same(got, oracle.emulate(m, xh), (m, pinned, "sum"))
+        got = api._host_pair(tfb.Method.TWOFOLD_FAST, xt[:0], None, dev, engine=eng)
+        assert got.tolist() == [0.0, 0.0]
+    xf = xh.astype(np.float32)
+    got = api._host_pair(tfb.Method.WIDE, torch.from_numpy(xf), None, dev, engine=eng)
+    _same(got, oracle.emulate(1, xf), "wide")
+    r = tfb.dot_twofold_fast(xh, yh)  # numpy inputs through the public wrapper (default engine)
     _same((r.value, r.error), oracle.emulate(2, xh, yh), "wrapper")
+    got = tfb.reduce(tfb.Method.KAHAN, torch.from_numpy(xh)).cpu().numpy()
+    _same(got, oracle.emulate(4, xh), "reduce host")
+    with pytest.raises(ValueError):  # mixed host/device operands are refused by the engine
+        lib = _lib.lib()
+        p = np.empty(2)
+        _lib.check(lib.tf_host_reduce(eng, 2, 1, xt.data_ptr(), torch.from_numpy(yh[:8]).cuda().data_ptr(), 8, 0,
+                                      p.ctypes.data))
 
 
 def test_shards_form_subtrees_of_single_gpu_tree(tfb, oracle, cuda):
