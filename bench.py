@@ -431,8 +431,9 @@ def run_ours(args):
         e2e = {"value": n * world * ke / wall / 1e9, "unit": UNIT, "h2d_bytes_per_step": bytes_per_step,
                "d2h_bytes_per_step": 16 if not rows else cfg.rows * item,
                "steps": ke, "ms_per_step": 1e3 * wall / ke,
-               "path": ("paper_1401_0248_b200.sharded_run(pinned host shard): leaf-aligned 64 MiB chunks "
-                        "H2D on a copy stream overlapped with the leaf kernels, tree kernel, D2H of the pair"),
+               "path": ("paper_1401_0248_b200.sharded_run(pinned host shard) -> C-ABI tf_host_reduce (host-buffer "
+                        "engine): leaf-aligned 16 MiB chunks DMA'd straight from the pinned shard on a copy stream, "
+                        "overlapped with the leaf kernels; tree kernel stores the pair into mapped host memory"),
                "timing": "wall clock around the steps after synchronize, max over ranks"}
 
     # --- CPU baseline (rank 0, N=1 only) ------------------------------------

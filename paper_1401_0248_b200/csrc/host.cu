@@ -9,9 +9,10 @@
 // tf_host_reduce(engine, method, dtype, hx, hy, n, leaf_log2, out_pair_host):
 //   * n fits one chunk: stage -> H2D per operand -> tf_reduce (fused; its
 //     last CTA stores the pair into mapped pinned memory) -> stream sync;
-//   * larger: leaf-aligned chunks; while the DMA engine moves chunk c and the
-//     GPU reduces its leaves (tf_reduce_leaves into partials + c*chunk_leaves),
-//     the pool copies chunk c+1 into the other pinned slot; tf_merge_tree
+//   * larger: leaf-aligned chunks; H2D copies on a copy stream, leaf kernels
+//     (tf_reduce_leaves into partials + c*chunk_leaves) on the compute stream,
+//     two slots: the DMA of chunk c+1 overlaps the leaves of chunk c, and the
+//     pool fills the other pinned slot meanwhile; tf_merge_tree
 //     closes the tree.  Chunks are whole leaves, so the partials and the tree
 //     are exactly those of tf_reduce on the whole array: bit-identical.
 //   * page-locked inputs (cudaHostAlloc / cudaHostRegister) skip the staging
@@ -151,10 +152,12 @@ Mem classify(const void* p) {
 struct HostEngine {
   int device = 0;
   size_t chunk = 0;  // bytes per operand per slot
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;   // kernels (and all work of single-chunk calls)
+  cudaStream_t cstream = nullptr;  // H2D copies of multi-chunk calls
   char* pin[2] = {nullptr, nullptr};  // [x | y] per slot
   char* dev[2] = {nullptr, nullptr};
-  cudaEvent_t h2d_done[2] = {nullptr, nullptr};
+  cudaEvent_t h2d_done[2] = {nullptr, nullptr};  // slot's DMA finished (pinned slot reusable)
+  cudaEvent_t k_done[2] = {nullptr, nullptr};    // slot's leaf kernel finished (device slot reusable)
   void* pair_pin = nullptr;  // mapped pinned: the last kernel stores the pair straight into it
   void* partials = nullptr;
   size_t partials_bytes = 0;
@@ -178,11 +181,13 @@ void release(HostEngine* g) {
     if (g->pin[b]) cudaFreeHost(g->pin[b]);
     if (g->dev[b]) cudaFree(g->dev[b]);
     if (g->h2d_done[b]) cudaEventDestroy(g->h2d_done[b]);
+    if (g->k_done[b]) cudaEventDestroy(g->k_done[b]);
   }
   if (g->pair_pin) cudaFreeHost(g->pair_pin);
   if (g->partials) cudaFree(g->partials);
   if (g->counters) cudaFree(g->counters);
   if (g->stream) cudaStreamDestroy(g->stream);
+  if (g->cstream) cudaStreamDestroy(g->cstream);
   delete g->pool;
   delete g;
 }
@@ -213,9 +218,9 @@ int ensure_scratch(HostEngine* g, size_t pb, int64_t cnt) {
 constexpr size_t kPiece = size_t(2) << 20;
 
 // Stage `bytes` of operand k (0 = x, 1 = y) from host `src` into device slot b.
-int stage(HostEngine* g, int b, int k, const char* src, size_t bytes, Mem kind, bool wait_slot) {
+int stage(HostEngine* g, cudaStream_t s, int b, int k, const char* src, size_t bytes, Mem kind, bool wait_slot) {
   char* d = g->dev[b] + k * g->chunk;
-  if (kind == Mem::kPinned) return cu(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, g->stream));
+  if (kind == Mem::kPinned) return cu(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s));
   if (wait_slot) {
     int rc = cu(cudaEventSynchronize(g->h2d_done[b]));  // the slot's previous DMA has drained
     if (rc) return rc;
@@ -225,7 +230,7 @@ int stage(HostEngine* g, int b, int k, const char* src, size_t bytes, Mem kind, 
   for (size_t off = 0; off < bytes; off += kPiece) {
     const size_t m = std::min(kPiece, bytes - off);
     g->pool->copy(p + off, src + off, m);
-    int rc = cu(cudaMemcpyAsync(d + off, p + off, m, cudaMemcpyHostToDevice, g->stream));
+    int rc = cu(cudaMemcpyAsync(d + off, p + off, m, cudaMemcpyHostToDevice, s));
     if (rc) return rc;
   }
   return TF_OK;
@@ -261,10 +266,12 @@ int tf_host_engine_create(int device, int threads, size_t chunk_bytes, void** en
     if (rc == TF_OK) rc = tfb::cu(e);
   };
   step(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+  step(cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking));
   for (int b = 0; b < 2 && rc == TF_OK; ++b) {
     step(cudaHostAlloc(reinterpret_cast<void**>(&g->pin[b]), 2 * chunk_bytes, cudaHostAllocDefault));
     step(cudaMalloc(reinterpret_cast<void**>(&g->dev[b]), 2 * chunk_bytes));
     step(cudaEventCreateWithFlags(&g->h2d_done[b], cudaEventDisableTiming));
+    step(cudaEventCreateWithFlags(&g->k_done[b], cudaEventDisableTiming));
   }
   step(cudaHostAlloc(&g->pair_pin, 16, cudaHostAllocMapped));
   if (rc != TF_OK) {
@@ -330,8 +337,8 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
     if (n <= chunk_elems) {
       const size_t bytes = n * item;
       if (n > 0) {
-        if ((rc = tfb::stage(g, 0, 0, cx, bytes, kx, true))) return rc;
-        if (dot && (rc = tfb::stage(g, 0, 1, cy, bytes, ky, true))) return rc;
+        if ((rc = tfb::stage(g, g->stream, 0, 0, cx, bytes, kx, true))) return rc;
+        if (dot && (rc = tfb::stage(g, g->stream, 0, 1, cy, bytes, ky, true))) return rc;
         if ((rc = tfb::cu(cudaEventRecord(g->h2d_done[0], g->stream)))) return rc;
       }
       rc = tf_reduce(method, dtype, g->dev[0], dot ? g->dev[0] + g->chunk : nullptr, n, lg, g->pair_pin,
@@ -343,17 +350,24 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
         const int64_t lo = c * chunk_elems;
         const int64_t m = std::min(n, lo + chunk_elems) - lo;
         const size_t bytes = m * item;
-        if ((rc = tfb::stage(g, b, 0, cx + lo * item, bytes, kx, c >= 2))) break;
-        if (dot && (rc = tfb::stage(g, b, 1, cy + lo * item, bytes, ky, c >= 2))) break;
-        if ((rc = tfb::cu(cudaEventRecord(g->h2d_done[b], g->stream)))) break;
+        // Copies on cstream, leaf kernels on stream: the DMA of chunk c+1 overlaps
+        // the leaves of chunk c.  Slot b is reused by chunk c+2 only after
+        // kernel c finished (device side) and DMA c drained (host side, pageable).
+        if (c >= 2 && (rc = tfb::cu(cudaStreamWaitEvent(g->cstream, g->k_done[b], 0)))) break;
+        if ((rc = tfb::stage(g, g->cstream, b, 0, cx + lo * item, bytes, kx, c >= 2))) break;
+        if (dot && (rc = tfb::stage(g, g->cstream, b, 1, cy + lo * item, bytes, ky, c >= 2))) break;
+        if ((rc = tfb::cu(cudaEventRecord(g->h2d_done[b], g->cstream)))) break;
+        if ((rc = tfb::cu(cudaStreamWaitEvent(g->stream, g->h2d_done[b], 0)))) break;
         rc = tf_reduce_leaves(method, dtype, g->dev[b], dot ? g->dev[b] + g->chunk : nullptr, m, lg,
                               static_cast<char*>(g->partials) + c * chunk_leaves * pair_bytes, g->stream);
+        if (rc == TF_OK) rc = tfb::cu(cudaEventRecord(g->k_done[b], g->stream));
       }
       if (rc == TF_OK)
         rc = tf_merge_tree(method, dtype, g->partials, leaves, g->pair_pin, g->stream);
     }
   }
   if (rc) {
+    cudaStreamSynchronize(g->cstream);
     cudaStreamSynchronize(g->stream);
     return rc;
   }
