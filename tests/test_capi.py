@@ -70,3 +70,20 @@ def test_workspace_size(lib):
     assert leaves == 1 and pb == 4 * 4096 * 16 and cnt == 4096  # wide pairs are binary64
     pb, cnt, leaves = workspace_size(Method.KAHAN, torch.float32, 1, 1 << 24)
     assert leaves == (1 << 24) >> 15 and pb == 4 * leaves * 8
+
+
+def test_host_engine_entry_points_without_gpu(lib):
+    """The host-buffer engine validates its handle and fails cleanly with no device."""
+    from paper_1401_0248_b200 import _lib
+    out = ctypes.c_double * 2
+    assert lib.tf_host_reduce(None, 2, 1, None, None, 0, 0, out()) == _lib.TF_EINVAL_ARG
+    assert lib.tf_host_engine_destroy(None) == _lib.TF_OK
+    assert lib.tf_host_engine_threads(None) == 0
+    eng = ctypes.c_void_p()
+    assert lib.tf_host_engine_create(0, 0, 0, None) == _lib.TF_EINVAL_ARG
+    rc = lib.tf_host_engine_create(0, 0, 0, ctypes.byref(eng))
+    if rc == _lib.TF_OK:  # a GPU is visible: clean up
+        assert lib.tf_host_engine_threads(eng) >= 1
+        assert lib.tf_host_engine_destroy(eng) == _lib.TF_OK
+    else:
+        assert rc in (_lib.TF_ECUDA, _lib.TF_EINVAL_ARG) and not eng.value
