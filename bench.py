@@ -435,6 +435,21 @@ def run_ours(args):
                         "engine): leaf-aligned 16 MiB chunks DMA'd straight from the pinned shard on a copy stream, "
                         "overlapped with the leaf kernels; tree kernel stores the pair into mapped host memory"),
                "timing": "wall clock around the steps after synchronize, max over ranks"}
+        # The link the e2e path streams over: plain pinned H2D of the same host
+        # buffer (up to 1 GiB, best of 3, CUDA events) — the e2e ceiling.
+        src = xh.view(-1).view(torch.uint8)[: 1 << 30]
+        dst = torch.empty_like(src, device=dev)
+        h2d = 0.0
+        for _ in range(3):
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record()
+            dst.copy_(src, non_blocking=True)
+            c1.record()
+            torch.cuda.synchronize()
+            h2d = max(h2d, src.numel() / (c0.elapsed_time(c1) * 1e-3) / 1e9)
+        del dst
+        e2e["h2d_link_gbs"] = h2d
+        e2e["frac_of_h2d_link"] = (bytes_per_step / (1e-3 * e2e["ms_per_step"]) / 1e9) / h2d
 
     # --- CPU baseline (rank 0, N=1 only) ------------------------------------
     cpu = None

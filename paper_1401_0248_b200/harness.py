@@ -73,7 +73,10 @@ _PAPER = {Method.DIRECT: "", Method.WIDE: "d", Method.TWOFOLD_FAST: "tf", Method
           Method.KAHAN: "k"}
 
 
-def memory_rows(precisions=("f32", "f64"), tiers=("small", "medium", "large"), reps: int = 20):
+def memory_rows(precisions=("f32", "f64"), tiers=("small", "medium", "large"), reps: int = 20,
+                methods=tuple(Method), ops=("sum", "dot"), flavor: Flavor = _CUDA, seed: int = 1):
+    """bench.run_bench (bench.py:196-247) on the device: every method x precision x
+    tier x op, graph-timed; data = the reference's LCG streams (x: NR, y: MMIX)."""
     rows = []
     dev = torch.device("cuda", torch.cuda.current_device())
     for prec in precisions:
@@ -81,14 +84,16 @@ def memory_rows(precisions=("f32", "f64"), tiers=("small", "medium", "large"), r
         item = torch.empty(0, dtype=dt).element_size()
         for tier in tiers:
             n = TIERS[tier] // item
-            x = lcg_fill("nr", n, 1, dt, device=dev)
-            y = lcg_fill("mmix", n, 2, dt, device=dev)
-            for method in Method:
+            x = lcg_fill("nr", n, seed, dt, device=dev)
+            y = lcg_fill("mmix", n, seed + 1, dt, device=dev) if "dot" in ops else None
+            for method in methods:
                 if method is Method.WIDE and prec != "f32":
                     continue
                 for op, yy in (("sum", None), ("dot", y)):
+                    if op not in ops:
+                        continue
                     out = torch.empty(2, dtype=torch.float64 if method is Method.WIDE else dt, device=dev)
-                    t = _graph_time(lambda: reduce(method, x, yy, out=out), reps)
+                    t = _graph_time(lambda: reduce(method, x, yy, flavor=flavor, out=out), reps)
                     nb = n * item * (1 if yy is None else 2)
                     rows.append(KernelRow(f"{op}{_PAPER[method]}", method.value, prec, tier, n, t, n / t / 1e9,
                                           nb / t / 1e9))
@@ -106,8 +111,9 @@ def read_roofs(rows):
     return out
 
 
-def noread_rows(precisions=("f32", "f64"), iters: int = 4096, reps: int = 5):
-    """p-rows: the recurrence on register-resident addends (compute roof)."""
+def noread_rows(precisions=("f32", "f64"), iters: int = 4096, reps: int = 5, methods=tuple(Method)):
+    """p-rows: the recurrence on register-resident addends (compute roof;
+    bench.run_noread_baseline, bench.py:281-307)."""
     rows = []
     dev = torch.device("cuda", torch.cuda.current_device())
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -115,7 +121,7 @@ def noread_rows(precisions=("f32", "f64"), iters: int = 4096, reps: int = 5):
     for prec in precisions:
         dt = DTYPES[prec]
         seed8 = torch.tensor([1.0 + 2.0 ** -(j + 3) for j in range(8)], dtype=dt, device=dev)
-        for method in Method:
+        for method in methods:
             if method is Method.WIDE and prec != "f32":
                 continue
             for op, dot in (("sum", 0), ("dot", 1)):
@@ -135,6 +141,66 @@ def noread_rows(precisions=("f32", "f64"), iters: int = 4096, reps: int = 5):
 def table1(reps: int = 20):
     mem = memory_rows(reps=reps)
     return mem + read_roofs(mem) + noread_rows()
+
+
+def rows_markdown(rows) -> str:
+    """One line per measurement (bench.bench_markdown analogue)."""
+    lines = ["| row | method | precision | tier | n | us | Gelem/s | GB/s |", "|---|---|---|---|---|---|---|---|"]
+    for r in rows:
+        lines.append(f"| {r.name} | {r.method} | {r.precision} | {r.tier} | {r.n} | {r.seconds * 1e6:.2f} | "
+                     f"{r.gelem_s:.2f} | {r.gbytes_s:.1f} |")
+    return "\n".join(lines) + "\n"
+
+
+def rows_csv(rows) -> str:
+    lines = ["row,method,precision,tier,n,seconds,gelem_s,gbytes_s"]
+    for r in rows:
+        lines.append(f"{r.name},{r.method},{r.precision},{r.tier},{r.n},{r.seconds!r},{r.gelem_s!r},{r.gbytes_s!r}")
+    return "\n".join(lines) + "\n"
+
+
+def run_selftest(pairs32: int = 10_000, pairs64: int = 2_000) -> list[str]:
+    """selftest.run_selftest (selftest.py:18-63) against the DEVICE code: the
+    strict-rounding canary, EFT exactness on random f32 / f64 pairs (vectorised
+    through tf_eft), and the LCG recurrence constants of the device generator.
+    Returns failure descriptions; empty means healthy."""
+    from fractions import Fraction
+
+    from .api import fast_two_sum, two_sum
+
+    failures = []
+    if lib().tf_canary() != _lib.TF_OK:
+        failures.append("device canary: fast_two_sum(1, 2**-53) lost its round-off or a product was fused "
+                        "into an FMA (value-unsafe code generation)")
+    g = np.random.default_rng(12345)
+    a32 = (g.uniform(-1, 1, pairs32) * 2.0 ** g.integers(-20, 20, pairs32)).astype(np.float32)
+    b32 = (g.uniform(-1, 1, pairs32) * 2.0 ** g.integers(-20, 20, pairs32)).astype(np.float32)
+    x, y = two_sum(a32, b32)
+    x, y = np.asarray(x), np.asarray(y)
+    bad = np.nonzero(x.astype(np.float64) + y.astype(np.float64) != a32.astype(np.float64) + b32.astype(np.float64))[0]
+    if bad.size:
+        i = int(bad[0])
+        failures.append(f"two_sum inexact for f32 pair ({a32[i]!r}, {b32[i]!r})")
+    swap = np.abs(a32) < np.abs(b32)
+    hi, lo = np.where(swap, b32, a32), np.where(swap, a32, b32)
+    xf, yf = (np.asarray(v) for v in fast_two_sum(hi, lo))
+    xt, yt = (np.asarray(v) for v in two_sum(hi, lo))
+    bad = np.nonzero((xf != xt) | (yf != yt))[0]
+    if bad.size:
+        i = int(bad[0])
+        failures.append(f"fast_two_sum disagrees with two_sum on ({hi[i]!r}, {lo[i]!r})")
+    a64 = g.uniform(-1, 1, pairs64) * 2.0 ** g.integers(-300, 300, pairs64)
+    b64 = g.uniform(-1, 1, pairs64) * 2.0 ** g.integers(-300, 300, pairs64)
+    x, y = (np.asarray(v) for v in two_sum(a64, b64))
+    for i in range(pairs64):
+        if Fraction(float(x[i])) + Fraction(float(y[i])) != Fraction(float(a64[i])) + Fraction(float(b64[i])):
+            failures.append(f"two_sum inexact for f64 pair ({a64[i]!r}, {b64[i]!r})")
+            break
+    nr = float(lcg_fill("nr", 1, 0, torch.float64)[0])
+    mx = float(lcg_fill("mmix", 1, 0, torch.float64)[0])
+    if nr != 1013904223 / 2.0 ** 32 or mx != float(1442695040888963407) / 2.0 ** 64:
+        failures.append("LCG recurrence constants are wrong")
+    return failures
 
 
 def format_table1(rows) -> str:
@@ -260,5 +326,6 @@ def run_scaling_study(ns=(10 ** 3, 10 ** 4, 10 ** 5, 10 ** 6, 10 ** 7), trials: 
     return out, slopes
 
 
-__all__ = ["KernelRow", "table1", "memory_rows", "noread_rows", "read_roofs", "format_table1", "AccuracyRow",
-           "Hours100Row", "run_accuracy_table", "run_hours100", "run_scaling_study"]
+__all__ = ["KernelRow", "table1", "memory_rows", "noread_rows", "read_roofs", "format_table1", "rows_markdown",
+           "rows_csv", "run_selftest", "AccuracyRow", "Hours100Row", "run_accuracy_table", "run_hours100",
+           "run_scaling_study"]
