@@ -101,10 +101,12 @@ int tf_leaf_log2(int dtype, int64_t n);
 int tf_set_leaf_split(int split);
 
 /* Tuning knob (process-wide): tail of the fused reduction — 0 = automatic
- * (PDL for the LDG loader; the TMA loader keeps its single launch), 1 =
- * last-CTA retire ticket inside the single launch, 2 = partials-only launch +
- * a programmatic-dependent-launch (PDL) tree kernel.  Identical results; env
- * TFB_TAIL sets the initial value. */
+ * (1-D inputs of <= 64 one-vector leaves: ONE thread-block-cluster launch whose
+ * CTAs merge through distributed shared memory; otherwise PDL for the LDG
+ * loader; the TMA loader keeps its single launch), 1 = last-CTA retire ticket
+ * inside the single launch, 2 = partials-only launch + a programmatic-
+ * dependent-launch (PDL) tree kernel.  Identical results; env TFB_TAIL sets
+ * the initial value. */
 int tf_set_tail(int tail);
 
 /* Human-readable description of the calling thread's last grid-reduction

@@ -457,6 +457,7 @@ __global__ void __launch_bounds__(kThreads) noread_kernel(const T* __restrict__ 
 
 }  // namespace tfb
 #include "tma.cuh"
+#include "small.cuh"
 namespace tfb {
 
 // ---------------------------------------------------------------------------
@@ -646,6 +647,47 @@ static int launch_leaves_tma(const T* px, const T* py, int64_t ldx, int64_t ldy,
   return check_launch();
 }
 
+// One cluster of max(1, P2/4) CTAs (small.cuh).  Cluster sizes above 8 are
+// opted into once per kernel and device.
+template <int M, typename T, bool DOT, bool VEC>
+static int launch_small(const T* px, const T* py, int64_t n, int64_t P, void* out, cudaStream_t stream) {
+  using A = typename Acc<M, T>::type;
+  auto kern = &small_cluster_kernel<M, T, DOT, VEC>;
+  int64_t P2 = 1;
+  while (P2 < P) P2 <<= 1;
+  const int C = static_cast<int>(P2 < kSmallLeaves ? 1 : P2 / kSmallLeaves);
+  if (C > 8) {
+    static std::mutex mu;
+    static std::unordered_map<int, bool> ok;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (!ok.count(dev)) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        return record_cuda_error();
+      ok[dev] = true;
+    }
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(C));
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(C);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  snprintf(g_last_launch, sizeof(g_last_launch),
+           "small_cluster_kernel<%s,%s,%s,%s> grid=%d cluster=%d block=%d leaves=%lld", method_tag(M),
+           sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", VEC ? "ldg128" : "scalar", C, C, kThreads,
+           static_cast<long long>(P));
+  if (cudaLaunchKernelEx(&cfg, kern, px, py, n, P, P2, static_cast<Pair<A>*>(out)) != cudaSuccess)
+    return record_cuda_error();
+  return check_launch();
+}
+
 template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1>
 static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                             int leaf_log2, int64_t P, void* partials, void* counters, void* out, int fused,
@@ -683,6 +725,12 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
                    (!DOT || (aligned16(y) && ((ldy * int64_t(sizeof(T))) % 16 == 0 || rows == 1)));
   auto px = static_cast<const T*>(x);
   auto py = static_cast<const T*>(y);
+  // Small 1-D inputs (one-vector leaves, <= 64 of them): a single cluster
+  // launch, no scratch, no tail kernel (small.cuh).  Auto tail only.
+  if (fused && !peer && rows == 1 && P <= kSmallMaxLeaves && tail_choice() == 0 &&
+      (int64_t(1) << leaf_log2) == int64_t(kThreads) * Vec<T>::V)
+    return vec ? launch_small<M, T, DOT, true>(px, py, cols, P, out, stream)
+               : launch_small<M, T, DOT, false>(px, py, cols, P, out, stream);
   // partial-pair capacity the kernels may write: callers of the leaves-only mode
   // (tf_reduce_leaves) promise ceil(n/L) pairs
   const int64_t cap = fused ? (partial_capacity < 0 ? 0 : partial_capacity) : units;

@@ -509,6 +509,45 @@ def test_pdl_tail_bit_identical(tfb, oracle, cuda):
         L.tf_set_leaf_split(0)
 
 
+def test_small_cluster_path_bit_identical(tfb, oracle, cuda):
+    """Single-cluster small path (<= 64 one-vector leaves, small.cuh) == emulator ==
+    PDL / ticket tails: every method, dtype, sum/dot, ragged sizes across every
+    cluster size (1..16 CTAs), 16-byte-misaligned (scalar) inputs, TwoProduct."""
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    try:
+        for dt in (np.float32, np.float64):
+            V = 4 if dt == np.float32 else 2
+            leaf = 256 * V
+            for n in (1, 5, leaf - 1, leaf, leaf + 3, 3 * leaf, 4 * leaf + 1, 9 * leaf - 7, 33 * leaf, 64 * leaf):
+                xh = oracle.lcg_fill("mmix", n + 1, 71, dt, True)
+                yh = oracle.lcg_fill("nr", n + 1, 72, dt, True)
+                xd, yd = torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda)
+                for off in (0, 1):  # off = 1: misaligned views take the scalar path
+                    x, y = xd[off:off + n], yd[off:off + n]
+                    xs, ys = xh[off:off + n], yh[off:off + n]
+                    for m in _methods(dt):
+                        meth = list(tfb.Method)[m]
+                        for dot in (False, True):
+                            want = oracle.emulate(m, xs, ys if dot else None)
+                            L.tf_set_tail(0)
+                            got = tfb.reduce(meth, x, y if dot else None).cpu().numpy()
+                            assert "small_cluster_kernel" in L.tf_last_launch().decode()
+                            _same(got, want, (dt, n, off, m, dot))
+                            for tail in (1, 2):
+                                L.tf_set_tail(tail)
+                                _same(tfb.reduce(meth, x, y if dot else None).cpu().numpy(), want,
+                                      (dt, n, off, m, dot, tail))
+                    L.tf_set_tail(0)
+                    for meth in (tfb.Method.TWOFOLD_FAST, tfb.Method.TWOFOLD_RIGOROUS):
+                        got = tfb.reduce(meth, x, y, track_product=True).cpu().numpy()
+                        L.tf_set_tail(2)
+                        _same(got, tfb.reduce(meth, x, y, track_product=True).cpu().numpy(), (dt, n, off, "tp"))
+                        L.tf_set_tail(0)
+    finally:
+        L.tf_set_tail(0)
+
+
 def test_gpu_exact_near_overflow(tfb, cuda):
     """Partial sums beyond binary64 range stay exact in the superaccumulator."""
     from fractions import Fraction
