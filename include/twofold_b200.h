@@ -267,11 +267,13 @@ int tf_host_engine_threads(const void* engine);
 /* (value, error) of x[, y] (n elements each) into out_pair_host (2 accumulator
  * elements, host memory); blocks until done.  Pageable inputs go through the
  * pinned slots (the pool copies chunk c+1 while chunk c is on the DMA engine
- * and its leaves reduce); page-locked inputs DMA directly; device pointers
- * reduce in place.  Leaf-aligned chunks: bit-identical to tf_reduce.  Calls on
- * one engine are serialised. */
+ * and its leaves reduce); page-locked inputs DMA directly; device pointers (of
+ * the engine's device) reduce in place.  after_stream (may be NULL): the
+ * stream device / page-locked operands are ordered on — the engine's work
+ * starts after that stream's pending work.  Leaf-aligned chunks: bit-identical
+ * to tf_reduce.  Calls on one engine are serialised. */
 int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const void* hy, int64_t n,
-                   int leaf_log2, void* out_pair_host);
+                   int leaf_log2, void* out_pair_host, void* after_stream);
 
 #ifdef __cplusplus
 }

@@ -326,9 +326,11 @@ def merge_pairs(method: Method, pairs: torch.Tensor, out: torch.Tensor | None = 
 
 def _host_pair(method: Method, x: torch.Tensor, y: torch.Tensor | None, dev: torch.device,
                leaf_log2: int = 0, track_product: bool = False, engine=None) -> np.ndarray:
-    """Grid flavor on HOST tensors through the native host-buffer engine
-    (tf_host_reduce, csrc/host.cu): pinned staging, leaf-aligned chunks whose
-    copies overlap the leaf kernels, blocking; bit-identical to the device path.
+    """Blocking grid flavor through the native host-buffer engine
+    (tf_host_reduce, csrc/host.cu).  Host tensors: pinned staging, leaf-aligned
+    chunks whose copies overlap the leaf kernels; CUDA tensors (of `dev`):
+    reduced in place after the current stream's pending work, the pair stored
+    straight into mapped host memory.  Bit-identical to the device path.
     Returns the raw (value, error) pair as a numpy array."""
     _lib.ensure_canary(dev.index)
     x = x.contiguous()
@@ -337,7 +339,7 @@ def _host_pair(method: Method, x: torch.Tensor, y: torch.Tensor | None, dev: tor
     eng = engine if engine is not None else _lib.host_engine(dev.index)
     check(lib().tf_host_reduce(eng, _mid(method, track_product, y is not None), _dtype_code(x.dtype),
                                x.data_ptr(), None if y is None else y.data_ptr(), x.numel(), leaf_log2,
-                               pair.ctypes.data), "tf_host_reduce")
+                               pair.ctypes.data, _stream_ptr(dev)), "tf_host_reduce")
     return pair
 
 
@@ -418,7 +420,8 @@ def run_flavor(method: Method, flavor: Flavor, data, b=None, *, track_product: b
         raise TypeError("wide accumulation is defined for float32 data only")
     if method not in _METHOD_ID:
         raise ValueError(f"unknown method {method!r}")
-    if flavor.kind == "cuda" and _all_host(x, y):  # host arrays: one blocking native call
+    if flavor.kind == "cuda" and (_all_host(x, y) or (x.is_cuda and (y is None or y.device == x.device))):
+        # one blocking native call (host or same-device operands)
         _mid(method, track_product, y is not None)
         pair = _host_pair(method, x, y, _device_for(x), track_product=track_product)
     else:
@@ -462,7 +465,7 @@ def _run_numpy(method: Method, a: np.ndarray, b: np.ndarray | None, track_produc
     _lib.ensure_canary(dev)
     pair = np.empty(2, dtype=np.float64 if method is Method.WIDE else a.dtype)
     check(lib().tf_host_reduce(_lib.host_engine(dev), mid, code, a.ctypes.data,
-                               None if b is None else b.ctypes.data, a.shape[0], 0, pair.ctypes.data),
+                               None if b is None else b.ctypes.data, a.shape[0], 0, pair.ctypes.data, None),
           "tf_host_reduce")
     if method in _TWOFOLD_METHODS:
         return SumResult(Twofold(pair[0], pair[1]), a.shape[0])

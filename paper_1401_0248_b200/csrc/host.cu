@@ -134,15 +134,16 @@ struct DeviceGuard {
   }
 };
 
-enum class Mem { kPageable, kPinned, kDevice };
+enum class Mem { kPageable, kPinned, kDevice, kOtherDevice };
 
-Mem classify(const void* p) {
+Mem classify(const void* p, int device) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return Mem::kPageable;
   }
-  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return Mem::kDevice;
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged)
+    return a.device == device ? Mem::kDevice : Mem::kOtherDevice;
   if (a.type == cudaMemoryTypeHost) return Mem::kPinned;
   return Mem::kPageable;
 }
@@ -158,6 +159,7 @@ struct HostEngine {
   char* dev[2] = {nullptr, nullptr};
   cudaEvent_t h2d_done[2] = {nullptr, nullptr};  // slot's DMA finished (pinned slot reusable)
   cudaEvent_t k_done[2] = {nullptr, nullptr};    // slot's leaf kernel finished (device slot reusable)
+  cudaEvent_t entry = nullptr;                   // the caller's stream at entry (device / pinned inputs)
   void* pair_pin = nullptr;  // mapped pinned: the last kernel stores the pair straight into it
   void* partials = nullptr;
   size_t partials_bytes = 0;
@@ -186,6 +188,7 @@ void release(HostEngine* g) {
   if (g->pair_pin) cudaFreeHost(g->pair_pin);
   if (g->partials) cudaFree(g->partials);
   if (g->counters) cudaFree(g->counters);
+  if (g->entry) cudaEventDestroy(g->entry);
   if (g->stream) cudaStreamDestroy(g->stream);
   if (g->cstream) cudaStreamDestroy(g->cstream);
   delete g->pool;
@@ -274,6 +277,7 @@ int tf_host_engine_create(int device, int threads, size_t chunk_bytes, void** en
     step(cudaEventCreateWithFlags(&g->k_done[b], cudaEventDisableTiming));
   }
   step(cudaHostAlloc(&g->pair_pin, 16, cudaHostAllocMapped));
+  step(cudaEventCreateWithFlags(&g->entry, cudaEventDisableTiming));
   if (rc != TF_OK) {
     tfb::release(g);
     return rc;
@@ -301,7 +305,7 @@ int tf_host_engine_threads(const void* engine) {
 }
 
 int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const void* hy, int64_t n,
-                   int leaf_log2, void* out_pair_host) {
+                   int leaf_log2, void* out_pair_host, void* after_stream) {
   if (!engine || !out_pair_host) return TF_EINVAL_ARG;
   if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
   if (n < 0) return TF_EINVAL_SHAPE;
@@ -321,8 +325,16 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
   const int lg = leaf_log2 ? leaf_log2 : tf_leaf_log2(dtype, n);
   if ((rc = tfb::ensure_scratch(g, std::max<size_t>(pb, pair_bytes), std::max<int64_t>(cnt, 1)))) return rc;
 
-  const tfb::Mem kx = n > 0 ? tfb::classify(hx) : tfb::Mem::kPageable;
-  const tfb::Mem ky = dot && n > 0 ? tfb::classify(hy) : kx;
+  const tfb::Mem kx = n > 0 ? tfb::classify(hx, g->device) : tfb::Mem::kPageable;
+  const tfb::Mem ky = dot && n > 0 ? tfb::classify(hy, g->device) : kx;
+  if (kx == tfb::Mem::kOtherDevice || ky == tfb::Mem::kOtherDevice) return TF_EINVAL_ARG;
+  // Device or page-locked operands may still be in flight on the caller's
+  // stream: order the engine's streams after it.
+  if (after_stream && (kx != tfb::Mem::kPageable || ky != tfb::Mem::kPageable)) {
+    if ((rc = tfb::cu(cudaEventRecord(g->entry, static_cast<cudaStream_t>(after_stream))))) return rc;
+    if ((rc = tfb::cu(cudaStreamWaitEvent(g->stream, g->entry, 0)))) return rc;
+    if ((rc = tfb::cu(cudaStreamWaitEvent(g->cstream, g->entry, 0)))) return rc;
+  }
   if (kx == tfb::Mem::kDevice && ky == tfb::Mem::kDevice) {  // already resident: plain tf_reduce
     rc = tf_reduce(method, dtype, hx, hy, n, leaf_log2, g->pair_pin, g->partials, g->partials_bytes,
                    g->counters, g->counters_len, g->stream);

@@ -36,9 +36,9 @@ for dt, lg in ((np.float32, 16), (np.float64, 16), (np.float64, 18), (np.float64
     pair = np.empty(2, dt)
     tag = f"{np.dtype(dt).name} 2^{lg} ({2 * xh.nbytes >> 10} KiB)"
     print(tag, "raw tf_host_reduce pageable: %.1f us" % per_call(
-        lambda: L.tf_host_reduce(eng, 2, code, xh.ctypes.data, yh.ctypes.data, n, 0, pair.ctypes.data)))
+        lambda: L.tf_host_reduce(eng, 2, code, xh.ctypes.data, yh.ctypes.data, n, 0, pair.ctypes.data, None)))
     print(tag, "raw tf_host_reduce pinned:   %.1f us" % per_call(
-        lambda: L.tf_host_reduce(eng, 2, code, xp.data_ptr(), yp.data_ptr(), n, 0, pair.ctypes.data)))
+        lambda: L.tf_host_reduce(eng, 2, code, xp.data_ptr(), yp.data_ptr(), n, 0, pair.ctypes.data, None)))
     print(tag, "public dot_twofold_fast numpy: %.1f us" % per_call(lambda: tfb.dot_twofold_fast(xh, yh)))
     xd = torch.empty(n, dtype=xp.dtype, device="cuda")
     yd = torch.empty_like(xd)
@@ -65,6 +65,6 @@ for lg in (20, 24, 26):
     pair = np.empty(2)
     for th in (1, 2, 4, 8, 12):
         e = _lib.host_engine(0, chunk_bytes=0, threads=th)
-        us = per_call(lambda: L.tf_host_reduce(e, 2, 1, xh.ctypes.data, yh.ctypes.data, n, 0, pair.ctypes.data),
+        us = per_call(lambda: L.tf_host_reduce(e, 2, 1, xh.ctypes.data, yh.ctypes.data, n, 0, pair.ctypes.data, None),
                       reps=max(3, (1 << 27) // n))
         print(f"f64 dot 2^{lg} pageable threads={th}: {us:9.1f} us {16 * n / us / 1e3:6.2f} GB/s", flush=True)

@@ -23,11 +23,18 @@ for _ in range(N):
 t1 = time.perf_counter()
 torch.cuda.synchronize()
 print(f"tfb.reduce (async, device tensors): {1e6 * (t1 - t0) / N:.1f} us host time per call")
+tfb.dot_twofold_fast(x, y)  # warm-up (creates the host engine)
 t0 = time.perf_counter()
 for _ in range(200):
     r = tfb.dot_twofold_fast(x, y)
 t1 = time.perf_counter()
 print(f"dot_twofold_fast (device tensors, returns numpy scalars): {1e6 * (t1 - t0) / 200:.1f} us per call")
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(200):
+    r = tfb.reduce(tfb.Method.TWOFOLD_FAST, x, y).cpu()
+t1 = time.perf_counter()
+print(f"reduce(...).cpu() (device tensors, async path + D2H): {1e6 * (t1 - t0) / 200:.1f} us per call")
 xh, yh = x.cpu().numpy(), y.cpu().numpy()
 t0 = time.perf_counter()
 for _ in range(200):

@@ -76,7 +76,7 @@ def test_host_engine_entry_points_without_gpu(lib):
     """The host-buffer engine validates its handle and fails cleanly with no device."""
     from paper_1401_0248_b200 import _lib
     out = ctypes.c_double * 2
-    assert lib.tf_host_reduce(None, 2, 1, None, None, 0, 0, out()) == _lib.TF_EINVAL_ARG
+    assert lib.tf_host_reduce(None, 2, 1, None, None, 0, 0, out(), None) == _lib.TF_EINVAL_ARG
     assert lib.tf_host_engine_destroy(None) == _lib.TF_OK
     assert lib.tf_host_engine_threads(None) == 0
     eng = ctypes.c_void_p()

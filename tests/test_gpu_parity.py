@@ -219,7 +219,7 @@ def test_streamed_host_path_equals_device_path(tfb, oracle, cuda):
         lib = _lib.lib()
         p = np.empty(2)
         _lib.check(lib.tf_host_reduce(eng, 2, 1, xt.data_ptr(), torch.from_numpy(yh[:8]).cuda().data_ptr(), 8, 0,
-                                      p.ctypes.data))
+                                      p.ctypes.data, None))
 
 
 def test_shards_form_subtrees_of_single_gpu_tree(tfb, oracle, cuda):
@@ -556,3 +556,26 @@ def test_gpu_exact_near_overflow(tfb, cuda):
         want = sum((Fraction(float(v)) for v in x), Fraction(0))
         assert got.fraction() == want
         assert got.hi == (float(want) if abs(want) < Fraction(2) ** 1024 else (np.inf if want > 0 else -np.inf))
+
+
+def test_blocking_wrappers_order_after_the_current_stream(tfb, oracle, cuda):
+    """run_flavor on CUDA tensors goes through tf_host_reduce on the engine's own
+    stream; it must start after the work pending on the caller's stream."""
+    n = 1 << 24
+    x = torch.zeros(n, dtype=torch.float32, device=cuda)
+    for _ in range(20):  # a queue of pending writes on the default stream
+        x.add_(0.5)
+    r = tfb.sum_twofold_fast(x)
+    assert float(r.value) + float(r.error) == 10.0 * n
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        y = torch.empty(n, dtype=torch.float64, device=cuda)
+        y.fill_(2.0)
+        for _ in range(10):
+            y.mul_(1.5)
+        r = tfb.dot_twofold_rigorous(y, y)
+    assert float(r.value) == n * (2.0 * 1.5 ** 10) ** 2
+    xh = oracle.lcg_fill("mmix", 70_001, 81, np.float64, True)
+    xd = torch.from_numpy(xh).to(cuda)
+    r = tfb.sum_twofold_fast(xd)
+    _same((r.value, r.error), oracle.emulate(2, xh), "device tensor wrapper")
