@@ -23,6 +23,7 @@ fallback: without the CUDA library or a GPU every compute call raises.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import functools
 import threading
@@ -236,6 +237,13 @@ def _stream_ptr(dev: torch.device) -> int:
     return torch.cuda.current_stream(dev).cuda_stream
 
 
+def _on(dev: torch.device):
+    """torch.cuda.device(dev), skipped when dev is already current (saves µs per call)."""
+    if dev.index == torch.cuda.current_device():
+        return contextlib.nullcontext()
+    return torch.cuda.device(dev)
+
+
 # ---------------------------------------------------------------------------
 # Per-(device, stream) scratch: grow-only partials + zeroed retire counters
 # (the kernels leave counters zero, so one buffer serves every call on a stream).
@@ -245,8 +253,11 @@ class _Scratch:
         self._lock = threading.Lock()
         self._bufs: dict[tuple[int, int], list] = {}
 
-    def get(self, dev: torch.device, partials_bytes: int, counters: int):
-        key = (dev.index, _stream_ptr(dev))
+    def get(self, dev: torch.device, partials_bytes: int, counters: int, stream_ptr: int | None = None):
+        key = (dev.index, _stream_ptr(dev) if stream_ptr is None else stream_ptr)
+        rec = self._bufs.get(key)
+        if rec is not None and rec[0].numel() >= partials_bytes and rec[1].numel() >= counters:
+            return rec[0], rec[1]
         with self._lock:
             rec = self._bufs.get(key)
             if rec is None:
@@ -294,11 +305,12 @@ def _reduce_grid(method: Method, x: torch.Tensor, y: torch.Tensor | None, leaf_l
         out = torch.empty(2, dtype=acc, device=dev)
     n = x.numel()
     pb, cnt, _ = workspace_size(method, x.dtype, 1, n, leaf_log2)
-    parts, ctrs = _scratch.get(dev, pb, cnt)  # cached per stream; also feeds leaf splitting
-    check(lib().tf_reduce(_mid(method, track_product, y is not None), _dtype_code(x.dtype), _ptr(x), _ptr(y), n,
-                          leaf_log2,
-                          out.data_ptr(), _ptr(parts), pb, _ptr(ctrs), cnt, _stream_ptr(dev)),
-          "tf_reduce")
+    sp = _stream_ptr(dev)
+    parts, ctrs = _scratch.get(dev, pb, cnt, sp)  # cached per stream; also feeds leaf splitting
+    rc = lib().tf_reduce(_mid(method, track_product, y is not None), _dtype_code(x.dtype), x.data_ptr(), _ptr(y), n,
+                         leaf_log2, out.data_ptr(), parts.data_ptr(), pb, ctrs.data_ptr(), cnt, sp)
+    if rc:
+        check(rc, "tf_reduce")
     return out
 
 
@@ -379,7 +391,7 @@ def reduce(method: Method, data, b=None, *, flavor: Flavor = _CUDA, leaf_log2: i
         raise TypeError("wide accumulation is defined for float32 data only")
     _mid(method, track_product, y is not None)  # validate before touching the device
     dev = _device_for(x)
-    with torch.cuda.device(dev):  # the C library launches on the current device
+    with _on(dev):  # the C library launches on the current device
         if flavor.kind == "cuda":
             if _all_host(x, y):
                 return _reduce_host(method, x, y, dev, leaf_log2, out, track_product)
