@@ -314,13 +314,6 @@ def _reduce_grid(method: Method, x: torch.Tensor, y: torch.Tensor | None, leaf_l
     return out
 
 
-def _reduce_leaves(method: Method, x: torch.Tensor, y: torch.Tensor | None, leaf_log2: int,
-                   partials_ptr: int, stream_ptr: int, track_product: bool = False) -> None:
-    check(lib().tf_reduce_leaves(_mid(method, track_product, y is not None), _dtype_code(x.dtype), _ptr(x),
-                                 _ptr(y), x.numel(),
-                                 leaf_log2, partials_ptr, stream_ptr), "tf_reduce_leaves")
-
-
 def merge_pairs(method: Method, pairs: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """Balanced TwoSum/Kahan/plain tree over a (k, 2) device tensor of pairs."""
     pairs = pairs.contiguous()
