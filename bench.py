@@ -64,8 +64,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0)
     ap.add_argument("--leaf-log2", type=int, default=0, help="override the auto leaf size (sweeps)")
     ap.add_argument("--graph", action="store_true", help="replay the timed steps from a CUDA graph")
-    ap.add_argument("--combine", default="nccl", choices=["nccl", "peer"],
-                    help="cross-rank combine: NCCL all-gather + merge kernel, or the fused NVLink peer combine")
+    ap.add_argument("--combine", default="auto", choices=["auto", "nccl", "peer"],
+                    help="cross-rank combine: fused NVLink peer combine (auto: after a one-time self-check "
+                         "against NCCL, else NCCL), or NCCL all-gather + merge kernel")
     ap.add_argument("--force-collective", action="store_true",
                     help="init NCCL and run the all-gather + merge path even at world size 1 (plumbing check)")
     return ap.parse_args()
@@ -285,6 +286,15 @@ def run_ours(args):
     copies = [(x, y)] + [(x.clone(), None if y is None else y.clone()) for _ in range(R - 1)]
     leaf_arg = args.leaf_log2 or lg
 
+    combine_desc = args.combine
+    if not rows and (world > 1 or args.force_collective):
+        acc_dt = torch.float64 if method is tfb.Method.WIDE else x.dtype
+        if args.combine == "auto":
+            combine_desc = (tfb.combine_in_use(None, dev, acc_dt) if world > 1 else
+                            "nccl (world size 1: the peer combine needs peers)")
+        combine_desc = {"peer": "fused NVLink peer combine inside the reduction launch (tf_reduce_peer)",
+                        "nccl": "NCCL all-gather of (v,e) pairs + tf_merge_tree"}.get(combine_desc, combine_desc)
+
     def step(i):
         xi, yi = copies[i % R]
         if rows:
@@ -477,7 +487,9 @@ def run_ours(args):
                        l2=(f"rotating over {R} input copies ({R * bytes_per_step / 1e6:.0f} MB >= 4x the 126 MB L2)"
                            if R > 1 else f"inputs {bytes_per_step / 2**30:.1f} GiB per rank >> 126 MB L2 (no flush)"),
                        leaf_log2=leaf_arg if not rows else (args.leaf_log2 or tfb.leaf_log2_for(x.dtype, cfg.cols)),
-                       steps_timing=("CUDA graph replay" if use_graph else "eager launches")),
+                       steps_timing=("CUDA graph replay" if use_graph else "eager launches"),
+                       **({"parallelism": f"dp{world}: contiguous shards; cross-rank combine: {combine_desc}"}
+                          if world > 1 or args.force_collective else {})),
         "hbm_gbs": bytes_per_step * world * K_eff / (t.item() * 1e-3) / 1e9,
         "steps_timed": K_eff,
         "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,

@@ -19,9 +19,14 @@ combine="peer" replaces reduce + NCCL all-gather + merge by ONE launch
 (tf_reduce_peer, csrc/peer.cuh): the CTA that builds the shard's root writes
 it into every peer's symmetric-memory buffer over NVLink, waits for the G
 pairs (system-scope release/acquire flags, epoch double-buffered, bounded
-spin) and merges them in-kernel.  It is opt-in: on this round's single-GPU
-pool it is verified at world size 1 (self-publication through the same code)
-and multi-GPU by construction; "nccl" stays the default.
+spin) and merges them in-kernel.  combine="auto" (the default) uses it for
+device-resident shards at world size > 1 after a one-time self-check: one
+peer combine on known per-rank data must equal the NCCL all-gather + merge
+bit for bit on every rank (all-reduce MIN of the verdicts, so all ranks pick
+the same path); otherwise — no symmetric memory / P2P, a mismatch, a peer
+timeout — it stays on NCCL and combine_in_use() says why.  On this round's
+single-GPU pool the peer kernel is verified at world size 1 (self-publication
+through the same code); multi-GPU by construction plus the self-check.
 """
 
 from __future__ import annotations
@@ -32,7 +37,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .api import Method, SumResult, Twofold, _TWOFOLD_METHODS, _np_type, leaf_log2_for, merge_pairs
+from .api import Method, SumResult, Twofold, _TWOFOLD_METHODS, _acc_dtype, _np_type, leaf_log2_for, merge_pairs
 
 LocalReduce = Callable[[Method, torch.Tensor, "torch.Tensor | None", int], torch.Tensor]
 Merge = Callable[[Method, torch.Tensor], torch.Tensor]
@@ -136,6 +141,60 @@ def _reduce_peer(method: Method, x: torch.Tensor, y, leaf_log2: int, group, trac
     return out
 
 
+_auto_cache: dict = {}
+
+
+def _peer_self_check(group, dev: torch.device, acc: torch.dtype) -> str | None:
+    """Run the fused peer combine once on known per-rank data and compare it with
+    the NCCL all-gather + merge result; every rank takes the same decision
+    (all-reduce MIN of the verdicts).  Returns None if the peer path is usable,
+    else the reason."""
+    from .api import _reduce_grid
+    rank, world = _world(group)
+    reason = None
+    try:
+        n = 3 * 4096 + 17
+        dt = torch.float32 if acc == torch.float32 else torch.float64
+        g = torch.Generator(device="cpu").manual_seed(1234 + rank)
+        x = (torch.rand(n, generator=g, dtype=torch.float64) * 2 - 1).to(dt).to(dev)
+        lg = leaf_log2_for(dt, n * world)
+        method = Method.TWOFOLD_RIGOROUS
+        with torch.cuda.device(dev):
+            got = _reduce_peer(method, x, None, lg, group, False)
+            local = _reduce_grid(method, x, None, lg)
+            parts = [torch.empty_like(local) for _ in range(world)]
+            dist.all_gather(parts, local, group=group)
+            want = _default_merge(method, torch.stack(parts, 0))
+            if not torch.equal(got.view(torch.int64 if dt == torch.float64 else torch.int32),
+                               want.view(torch.int64 if dt == torch.float64 else torch.int32)):
+                reason = "peer self-check result differs from the NCCL combine"
+            elif peer_combine_error(group):
+                reason = "peer self-check timed out waiting for a peer"
+    except Exception as exc:  # no symmetric memory / P2P on this box
+        reason = f"peer combine unavailable: {type(exc).__name__}: {exc}"
+    return _agree(reason, group, dev)
+
+
+def _agree(reason: str | None, group, dev: torch.device) -> str | None:
+    """Every rank adopts the peer combine only if every rank's check passed."""
+    ok = torch.tensor([0 if reason else 1], dtype=torch.int32, device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+    if reason is None and int(ok.item()) == 0:
+        reason = "peer self-check failed on another rank"
+    return reason
+
+
+def combine_in_use(group=None, dev: torch.device | None = None, acc: torch.dtype = torch.float64) -> str:
+    """The cross-rank combine `combine="auto"` picks for this group/device/accumulator:
+    "peer" (fused NVLink combine, self-checked against NCCL once) or "nccl (<reason>)"."""
+    dev = dev or torch.device("cuda", torch.cuda.current_device())
+    key = (id(group), dev.index, acc)
+    if key not in _auto_cache:
+        _auto_cache[key] = _peer_self_check(group, dev, acc)
+    reason = _auto_cache[key]
+    return "peer" if reason is None else f"nccl ({reason})"
+
+
 def peer_combine_error(group=None) -> bool:
     """True if any peer combine on this rank timed out waiting for a peer (result NaN)."""
     return any(int(pc.error.item()) != 0 for (gid, _, _), pc in _peer_cache.items() if gid == id(group))
@@ -151,18 +210,26 @@ def sharded_reduce(method: Method, x_local: torch.Tensor, y_local: torch.Tensor 
                    n_global: int, leaf_log2: int = 0, group=None,
                    local_reduce: LocalReduce | None = None, merge: Merge | None = None,
                    track_product: bool = False, force_collective: bool = False,
-                   combine: str = "nccl") -> torch.Tensor:
+                   combine: str = "auto") -> torch.Tensor:
     """Raw (value, error) pair of the global array, identical on every rank.
 
     x_local / y_local: this rank's shard (CUDA tensors for the default
     reducer).  leaf_log2 = 0 uses the global array's auto leaf size, so the
-    partition does not depend on G.  combine: "nccl" (all-gather + merge
-    kernel) or "peer" (fused NVLink combine inside the reduction launch).
+    partition does not depend on G.  combine: "peer" (fused NVLink combine
+    inside the reduction launch), "nccl" (all-gather + merge kernel), or
+    "auto" (default: peer for device-resident shards at world size > 1 once a
+    one-time self-check against NCCL passed on every rank, else nccl).
     """
-    if combine not in ("nccl", "peer"):
-        raise ValueError("combine must be 'nccl' or 'peer'")
+    if combine not in ("nccl", "peer", "auto"):
+        raise ValueError("combine must be 'auto', 'nccl' or 'peer'")
     lg = leaf_log2 or leaf_log2_for(x_local.dtype, n_global)
-    if combine == "peer" and dist.is_available() and dist.is_initialized() and local_reduce is None:
+    distributed = dist.is_available() and dist.is_initialized()
+    if combine == "auto":
+        combine = "nccl"
+        if (distributed and local_reduce is None and merge is None and x_local.is_cuda and _world(group)[1] > 1
+                and combine_in_use(group, x_local.device, _acc_dtype(method, x_local.dtype)) == "peer"):
+            combine = "peer"
+    if combine == "peer" and distributed and local_reduce is None:
         if not x_local.is_cuda:
             raise ValueError("the peer combine reduces device-resident shards")
         return _reduce_peer(method, x_local, y_local, lg, group, track_product)

@@ -43,6 +43,14 @@ def main():
                              track_product=True).cpu()
     assert torch.equal(got, ref)
     assert not tdist.peer_combine_error()
+    # combine="auto": the one-time self-check (peer vs NCCL on known data) passes on every rank
+    for acc in (torch.float32, torch.float64):
+        used = tfb.combine_in_use(None, dev, acc)
+        assert used == "peer", used
+    if world > 1:  # auto then routes device shards through the fused kernel
+        got = tfb.sharded_reduce(tfb.Method.TWOFOLD_FAST, x, y, n_global=n_global).cpu()
+        ref = tfb.sharded_reduce(tfb.Method.TWOFOLD_FAST, x, y, n_global=n_global, combine="nccl").cpu()
+        assert torch.equal(got, ref)
     dist.barrier()
     dist.destroy_process_group()
     if rank == 0:

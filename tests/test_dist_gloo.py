@@ -102,6 +102,36 @@ def test_sharded_equals_single_device_tree(oracle, world, dtype_name):
         assert adds == n
 
 
+def _agree_worker(rank, world, port, q):
+    sys.path.insert(0, REPO)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1401_0248_b200 import dist as D
+    cpu = torch.device("cpu")
+    all_ok = D._agree(None, None, cpu)
+    one_bad = D._agree("boom" if rank == 1 else None, None, cpu)
+    q.put((rank, all_ok, one_bad))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_auto_combine_decision_is_collective():
+    """combine="auto": one rank's failed peer self-check moves EVERY rank to NCCL."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = dict((r, (a, b)) for r, a, b in (q.get(timeout=300) for _ in range(3)))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert all(a is None for a, _ in res.values())
+    assert res[1][1] == "boom"
+    assert res[0][1] == res[2][1] == "peer self-check failed on another rank"
+
+
 def test_ragged_shards_cover_everything(oracle):
     """Non-power-of-two n: shards are leaf-aligned and the merged pair still tracks the exact sum."""
     n = 300_007
