@@ -49,3 +49,13 @@ def test_hours100_seq_reproduces_reference_goldens(cuda, golden, capsys):
         assert float(got[1]) == float.fromhex(g["deviation_hours"]), g["method"]
         if g["estimate_hours"] is not None:
             assert float(got[2]) == float.fromhex(g["estimate_hours"]), g["method"]
+
+
+@pytest.mark.gpu
+def test_no_meta_reruns_are_byte_identical(cuda, capsys):
+    """cli.py:120-132 / test_cli.py:33-36: '#' metadata suppressed -> identical reports."""
+    argv = ["accuracy", "--n", "50000", "--precision", "f64", "--format", "csv", "--no-meta"]
+    assert main(argv) == 0
+    first = capsys.readouterr().out
+    assert main(argv) == 0
+    assert capsys.readouterr().out == first and first.count("\n") == 1 + 2 * 2 * 3
