@@ -27,7 +27,18 @@ namespace tfb {
 
 constexpr int kExactThreads = 256;
 constexpr int kLimbs = 72;   // 72 * 32 = 2304 bit positions >= 2098 + 64 carry bits
-constexpr int kExpK = 4;     // per-thread expansion length
+#ifndef TFB_EXACT_K
+#define TFB_EXACT_K 4
+#endif
+#ifndef TFB_EXACT_DUAL
+#define TFB_EXACT_DUAL 0
+#endif
+#ifndef TFB_EXACT_MINB
+#define TFB_EXACT_MINB 4
+#endif
+constexpr int kExactMinBlocks = TFB_EXACT_MINB;  // CTAs per SM (register cap) and grid = SMs x this
+constexpr int kExpK = TFB_EXACT_K;        // per-thread expansion length
+constexpr int kExpN = 1 + TFB_EXACT_DUAL;  // independent expansions per thread (ILP)
 
 // One CTA record: kLimbs normalised digits in [0, 2^32) + a signed top carry,
 // + a non-finite counter.
@@ -72,14 +83,17 @@ __device__ __forceinline__ void cascade(double (&a)[kExpK], double x, long long*
     deposit(acc, x);
     return;
   }
+  // Early exit: once a TwoSum is exact nothing is left to carry (typical data
+  // settles after two components, halving the FP64 work per addend).
 #pragma unroll
   for (int i = 0; i < kExpK; ++i) {
     double s, e;
     two_sum<double>(a[i], x, s, e);
     a[i] = s;
     x = e;
+    if (x == 0.0) return;
   }
-  if (x != 0.0) deposit(acc, x);
+  deposit(acc, x);
 }
 
 template <typename T> struct ExVec;
@@ -95,30 +109,34 @@ __device__ __forceinline__ double ex_get(const double2& v, int j) { return j == 
 // Addends: 0 = x_i, 1 = fl_T(x_i*y_i) (the twofold kernels' addends), 2 = exact
 // products (fl(x*y) and fma(x, y, -fl(x*y)) for binary64; exact in binary64 for
 // binary32 data).  abs: |addend| (A = sum |y_i| of the tolerances).
-template <typename T>
-__device__ __forceinline__ void add_element(double (&a)[kExpK], long long* acc, T xv, T yv, int mode,
-                                            bool absval, int& nonfinite) {
+// MODE / ABS are template parameters: the per-element path has no runtime
+// branches besides the cascade's early exit.
+template <typename T, int MODE, bool ABS>
+__device__ __forceinline__ void add_element(double (&a)[kExpK], long long* acc, T xv, T yv, int& nonfinite) {
+  constexpr bool kResidual = MODE == 2 && sizeof(T) == 8;  // binary64 true products carry fma residuals
   double p, r = 0.0;
-  if (mode == 0) {
+  if constexpr (MODE == 0) {
     p = static_cast<double>(xv);
-  } else if (mode == 1) {
+  } else if constexpr (MODE == 1) {
     p = static_cast<double>(Ar<T>::mul(xv, yv));
-  } else if (sizeof(T) == 4) {
-    p = __dmul_rn(static_cast<double>(xv), static_cast<double>(yv));  // exact
   } else {
-    p = __dmul_rn(static_cast<double>(xv), static_cast<double>(yv));
-    r = __fma_rn(static_cast<double>(xv), static_cast<double>(yv), -p);
+    p = __dmul_rn(static_cast<double>(xv), static_cast<double>(yv));  // exact for binary32 data
+    if constexpr (kResidual) r = __fma_rn(static_cast<double>(xv), static_cast<double>(yv), -p);
   }
-  if (!isfinite(p) || !isfinite(r)) {
+  if (!isfinite(p) || (kResidual && !isfinite(r))) {
     ++nonfinite;
     return;
   }
-  if (absval && p < 0.0) {  // |p + r| = -(p + r) when p < 0 (|r| <= ulp(p)/2)
-    p = -p;
-    r = -r;
+  if constexpr (ABS) {
+    if (p < 0.0) {  // |p + r| = -(p + r) when p < 0 (|r| <= ulp(p)/2)
+      p = -p;
+      r = -r;
+    }
   }
   cascade(a, p, acc);
-  if (r != 0.0) cascade(a, r, acc);
+  if constexpr (kResidual) {
+    if (r != 0.0) cascade(a, r, acc);
+  }
 }
 
 // Normalise limbs (digits -> [0, 2^32), signed carry out) by one thread.
@@ -249,20 +267,23 @@ __device__ __noinline__ void finish(long long* tot, double* out, long long* limb
   *counter = 0u;  // leave the workspace reusable
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kExactThreads, 4) exact_kernel(
-    const T* __restrict__ x, const T* __restrict__ y, int64_t n, int mode, int absval,
+template <typename T, int MODE, bool ABS>
+__global__ void __launch_bounds__(kExactThreads, kExactMinBlocks) exact_kernel(
+    const T* __restrict__ x, const T* __restrict__ y, int64_t n,
     ExactRecord* __restrict__ records, unsigned* __restrict__ counter, double* __restrict__ out,
     long long* __restrict__ limbs_out) {
+  constexpr bool DOT = MODE != 0;
   __shared__ long long acc[kLimbs];
   __shared__ int s_last;
   __shared__ int s_nonfinite;
   for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) acc[k] = 0;
   if (threadIdx.x == 0) s_nonfinite = 0;
   __syncthreads();
-  double a[kExpK];
+  double a[kExpN][kExpK];
 #pragma unroll
-  for (int i = 0; i < kExpK; ++i) a[i] = 0.0;
+  for (int q = 0; q < kExpN; ++q)
+#pragma unroll
+    for (int i = 0; i < kExpK; ++i) a[q][i] = 0.0;
   int nonfinite = 0;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t gtid = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
@@ -272,7 +293,7 @@ __global__ void __launch_bounds__(kExactThreads, 4) exact_kernel(
   constexpr int VB = ExVec<T>::V;
   constexpr int U = 2;
   const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
-                       (y == nullptr || (reinterpret_cast<uintptr_t>(y) & 15u) == 0);
+                       (!DOT || (reinterpret_cast<uintptr_t>(y) & 15u) == 0);
   int64_t scalar_from = 0;
   if (aligned) {
     const int64_t nv = n / VB;
@@ -284,28 +305,31 @@ __global__ void __launch_bounds__(kExactThreads, 4) exact_kernel(
 #pragma unroll
       for (int k = 0; k < U; ++k) {
         va[k] = ex_ld(xv + v + k * stride);
-        if (y) vb[k] = ex_ld(yv + v + k * stride);
+        if constexpr (DOT) vb[k] = ex_ld(yv + v + k * stride);
       }
 #pragma unroll
       for (int k = 0; k < U; ++k)
 #pragma unroll
         for (int j = 0; j < VB; ++j)
-          add_element<T>(a, acc, ex_get(va[k], j), y ? ex_get(vb[k], j) : T(0), mode, absval != 0, nonfinite);
+          add_element<T, MODE, ABS>(a[j % kExpN], acc, ex_get(va[k], j), DOT ? ex_get(vb[k], j) : T(0),
+                                    nonfinite);
     }
     for (; v < nv; v += stride) {
       const VT va = ex_ld(xv + v);
       VT vb;
-      if (y) vb = ex_ld(yv + v);
+      if constexpr (DOT) vb = ex_ld(yv + v);
 #pragma unroll
       for (int j = 0; j < VB; ++j)
-        add_element<T>(a, acc, ex_get(va, j), y ? ex_get(vb, j) : T(0), mode, absval != 0, nonfinite);
+        add_element<T, MODE, ABS>(a[j % kExpN], acc, ex_get(va, j), DOT ? ex_get(vb, j) : T(0), nonfinite);
     }
     scalar_from = nv * VB;
   }
   for (int64_t i = scalar_from + gtid; i < n; i += stride)
-    add_element<T>(a, acc, x[i], y ? y[i] : T(0), mode, absval != 0, nonfinite);
+    add_element<T, MODE, ABS>(a[0], acc, x[i], DOT ? y[i] : T(0), nonfinite);
 #pragma unroll
-  for (int i = 0; i < kExpK; ++i) deposit(acc, a[i]);
+  for (int q = 0; q < kExpN; ++q)
+#pragma unroll
+    for (int i = 0; i < kExpK; ++i) deposit(acc, a[q][i]);
   if (nonfinite) atomicAdd(&s_nonfinite, nonfinite);
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -345,7 +369,7 @@ extern "C" {
 int tf_exact_workspace(int64_t* records, size_t* bytes) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t g = static_cast<int64_t>(sms) * 4;
+  const int64_t g = static_cast<int64_t>(sms) * kExactMinBlocks;
   if (records) *records = g;
   if (bytes) *bytes = static_cast<size_t>(g) * sizeof(ExactRecord);
   return TF_OK;
@@ -366,17 +390,25 @@ int tf_exact(int dtype, const void* x, const void* y, int64_t n, int flags, void
   if (g < 1) g = 1;
   if (!records || records_bytes < static_cast<size_t>(g) * sizeof(ExactRecord)) return TF_EWORKSPACE;
   auto s = static_cast<cudaStream_t>(stream);
-  const int absval = (flags & TF_EXACT_ABS) ? 1 : 0;
-  if (dtype == TF_F32)
-    exact_kernel<float><<<static_cast<unsigned>(g), kExactThreads, 0, s>>>(
-        static_cast<const float*>(x), static_cast<const float*>(y), n, mode, absval,
-        static_cast<ExactRecord*>(records), static_cast<unsigned*>(counter), static_cast<double*>(out2),
-        static_cast<long long*>(limbs_out));
-  else
-    exact_kernel<double><<<static_cast<unsigned>(g), kExactThreads, 0, s>>>(
-        static_cast<const double*>(x), static_cast<const double*>(y), n, mode, absval,
-        static_cast<ExactRecord*>(records), static_cast<unsigned*>(counter), static_cast<double*>(out2),
-        static_cast<long long*>(limbs_out));
+  const bool absval = (flags & TF_EXACT_ABS) != 0;
+  const dim3 grid(static_cast<unsigned>(g));
+  auto* rec = static_cast<ExactRecord*>(records);
+  auto* ctr = static_cast<unsigned*>(counter);
+  auto* o = static_cast<double*>(out2);
+  auto* lo = static_cast<long long*>(limbs_out);
+#define TFB_EXACT(T, MODE, ABS)                                                                            \
+  exact_kernel<T, MODE, ABS><<<grid, kExactThreads, 0, s>>>(static_cast<const T*>(x), static_cast<const T*>(y), \
+                                                           n, rec, ctr, o, lo)
+#define TFB_EXACT_T(T)                                                                                     \
+  do {                                                                                                     \
+    if (mode == 0) { if (absval) TFB_EXACT(T, 0, true); else TFB_EXACT(T, 0, false); }                   \
+    else if (mode == 1) { if (absval) TFB_EXACT(T, 1, true); else TFB_EXACT(T, 1, false); }              \
+    else { if (absval) TFB_EXACT(T, 2, true); else TFB_EXACT(T, 2, false); }                             \
+  } while (0)
+  if (dtype == TF_F32) TFB_EXACT_T(float);
+  else TFB_EXACT_T(double);
+#undef TFB_EXACT_T
+#undef TFB_EXACT
   return check_launch();
 }
 
