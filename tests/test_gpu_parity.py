@@ -579,3 +579,38 @@ def test_blocking_wrappers_order_after_the_current_stream(tfb, oracle, cuda):
     xd = torch.from_numpy(xh).to(cuda)
     r = tfb.sum_twofold_fast(xd)
     _same((r.value, r.error), oracle.emulate(2, xh), "device tensor wrapper")
+
+
+def test_thread_safety_many_streams(tfb, oracle, cuda):
+    """The reference's functions are pure and thread-safe: several host
+    threads, each on its own CUDA stream (own scratch) plus the shared host engine,
+    get bit-identical results to a single-threaded run."""
+    import threading
+    sizes = (5_001, 70_001, (1 << 20) + 3)
+    data = {}
+    for n in sizes:
+        xh = oracle.lcg_fill("mmix", n, 91, np.float64, True)
+        yh = oracle.lcg_fill("nr", n, 92, np.float64, True)
+        data[n] = (xh, yh, torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda), oracle.emulate(2, xh, yh))
+    errors = []
+
+    def worker(k):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for it in range(40):
+                    n = sizes[(k + it) % len(sizes)]
+                    xh, yh, xd, yd, want = data[n]
+                    got = tfb.reduce(tfb.Method.TWOFOLD_FAST, xd, yd).cpu().numpy()
+                    assert float(got[0]).hex() == float(want[0]).hex() and float(got[1]).hex() == float(want[1]).hex()
+                    r = tfb.dot_twofold_fast(xh, yh)  # numpy: the shared host engine
+                    assert float(r.value).hex() == float(want[0]).hex() and float(r.error).hex() == float(want[1]).hex()
+        except Exception as exc:  # surfaced in the main thread
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors[:3]
