@@ -614,3 +614,51 @@ def test_thread_safety_many_streams(tfb, oracle, cuda):
     for t in threads:
         t.join()
     assert not errors, errors[:3]
+
+
+def _same_nf(got, want, ctx):
+    """Bit-exact, except that every NaN matches every NaN (payload/sign of a
+    generated NaN is implementation-defined: x86 0xFFF8..., CUDA 0x7FFF...)."""
+    for g, w in zip((float(got[0]), float(got[1])), (float(want[0]), float(want[1]))):
+        if np.isnan(w):
+            assert np.isnan(g), (ctx, got, want)
+        else:
+            assert g.hex() == w.hex(), (ctx, got, want)
+
+
+def test_non_finite_inputs_grid_and_seq(tfb, oracle, cuda):
+    """inf / -inf / NaN addends and overflowing products propagate exactly as in the
+    reference recurrence (seq flavor vs the oracle's restatement) and as in the
+    GPU tree (grid flavor vs the emulator), for every method."""
+    rng = np.random.default_rng(7)
+    for dt in (np.float32, np.float64):
+        big = np.finfo(dt).max
+        for n in (37, 5_001, 200_003):
+            base = rng.uniform(-1, 1, n).astype(dt)
+            cases = []
+            for pat in ("inf", "ninf", "both", "nan", "ovf"):
+                x = base.copy()
+                y = rng.uniform(-1, 1, n).astype(dt)
+                if pat == "inf":
+                    x[n // 3] = np.inf
+                elif pat == "ninf":
+                    x[n // 2] = -np.inf
+                elif pat == "both":
+                    x[1], x[n - 2] = np.inf, -np.inf
+                elif pat == "nan":
+                    x[n // 5] = np.nan
+                else:  # finite inputs whose sum / products overflow
+                    x[:4] = big
+                    y[:4] = dt(4)
+                cases.append((pat, x, y))
+            for pat, x, y in cases:
+                xd, yd = torch.from_numpy(x).to(cuda), torch.from_numpy(y).to(cuda)
+                for m in _methods(dt):
+                    meth = list(tfb.Method)[m]
+                    for dot in (False, True):
+                        yy, yyh = (yd, y) if dot else (None, None)
+                        _same_nf(tfb.reduce(meth, xd, yy).cpu().numpy(), oracle.emulate(m, x, yyh),
+                                 (dt, n, pat, m, dot, "grid"))
+                        if n <= 5_001:
+                            seq = tfb.reduce(meth, xd, yy, flavor=tfb.Flavor.sequential()).cpu().numpy()
+                            _same_nf(seq, oracle.seq(m, x, yyh), (dt, n, pat, m, dot, "seq"))
