@@ -28,9 +28,10 @@ def make(O, spec):
     raise ValueError(kind)
 
 
-def load_inputs(O, golden):
+def load_inputs(O, golden, section=None):
     out = {}
-    for name, rec in golden["inputs"].items():
+    recs = golden["inputs"] if section is None else golden[section]["inputs"]
+    for name, rec in recs.items():
         x = make(O, rec["x"])
         y = make(O, rec["y"])
         out[name] = (x, y)

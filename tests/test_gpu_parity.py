@@ -105,6 +105,16 @@ def test_dot_by_ones_equals_sum_bitwise(tfb, oracle, cuda):
     assert tfb.dot_wide(x, ones).value == tfb.sum_wide(x).value
 
 
+def test_non_finite_flavors_match_reference(tfb, oracle, golden):
+    """GPU seq / unroll:k / vec on inf / -inf / NaN / overflow inputs == the
+    reference's run_flavor (tests/golden nonfinite section; NaN == NaN)."""
+    inputs = load_inputs(oracle, golden, "nonfinite")
+    for case in golden["nonfinite"]["cases"]:
+        x, y = inputs[case["input"]]
+        r = tfb.run_flavor(tfb.Method(case["method"]), tfb.Flavor.parse(case["flavor"]), x, y)
+        assert _hex(r.value) == case["value"] and _hex(r.error) == case["error"], case
+
+
 def test_seq_and_lane_flavors_bit_exact_with_reference(tfb, oracle, golden):
     """GPU seq / unroll:k / vec == the reference's own run_flavor output (fixtures)."""
     inputs = load_inputs(oracle, golden)

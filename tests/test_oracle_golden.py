@@ -152,3 +152,20 @@ def test_threads_baseline_tracks_exact(oracle, inputs):
     for nt in (2, 3, 8):
         v, e = oracle.threads(3, x, y, nt)
         assert oracle.deviation(v, e, S) <= oracle.bound(3, np.float64, len(x), A)
+
+
+def test_non_finite_seq_and_lanes_match_reference(oracle, golden):
+    """inf / -inf / NaN / overflow inputs: the oracle's seq and lane kernels propagate
+    exactly as the reference's run_flavor (every NaN equal to every NaN)."""
+    from golden_inputs import load_inputs
+    inputs = load_inputs(oracle, golden, "nonfinite")
+    for case in golden["nonfinite"]["cases"]:
+        x, y = inputs[case["input"]]
+        m = METHOD_ID[case["method"]]
+        k = _flavor_lanes(case["flavor"], x.dtype)
+        with np.errstate(all="ignore"):
+            v, e = oracle.seq(m, x, y) if k == 0 else oracle.lanes(m, x, y, k)
+        if m in (0, 1, 4):
+            e = type(v)(0)
+        assert float(v).hex() == case["value"] and float(e).hex() == case["error"], case
+    assert len(golden["nonfinite"]["cases"]) == 324
