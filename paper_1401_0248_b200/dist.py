@@ -224,14 +224,21 @@ def sharded_reduce(method: Method, x_local: torch.Tensor, y_local: torch.Tensor 
         raise ValueError("combine must be 'auto', 'nccl' or 'peer'")
     lg = leaf_log2 or leaf_log2_for(x_local.dtype, n_global)
     distributed = dist.is_available() and dist.is_initialized()
+    # The peer combine's epoch is a host counter baked into each launch, so a
+    # captured CUDA graph would replay a stale epoch: never inside a capture.
+    capturing = x_local.is_cuda and torch.cuda.is_current_stream_capturing()
     if combine == "auto":
         combine = "nccl"
-        if (distributed and local_reduce is None and merge is None and x_local.is_cuda and _world(group)[1] > 1
+        if (distributed and local_reduce is None and merge is None and x_local.is_cuda and not capturing
+                and _world(group)[1] > 1
                 and combine_in_use(group, x_local.device, _acc_dtype(method, x_local.dtype)) == "peer"):
             combine = "peer"
     if combine == "peer" and distributed and local_reduce is None:
         if not x_local.is_cuda:
             raise ValueError("the peer combine reduces device-resident shards")
+        if capturing:
+            raise ValueError("the peer combine is not CUDA-graph capturable (host-side epochs); "
+                             "use combine='auto' or 'nccl' inside a capture")
         return _reduce_peer(method, x_local, y_local, lg, group, track_product)
     if local_reduce is None:
         local = _default_local(method, x_local, y_local, lg, track_product)
