@@ -143,11 +143,14 @@ def host_engine(device_index: int, chunk_bytes: int | None = None, threads: int 
     key = (device_index, chunk_bytes, threads)
     eng = _engines.get(key)
     if eng is None:
+        L = lib()  # load outside _lock: lib() takes the same (non-reentrant) lock on first use
         with _lock:
             eng = _engines.get(key)
             if eng is None:
                 eng = ctypes.c_void_p()
-                check(lib().tf_host_engine_create(device_index, threads, chunk_bytes, ctypes.byref(eng)),
-                      "tf_host_engine_create")
+                rc = L.tf_host_engine_create(device_index, threads, chunk_bytes, ctypes.byref(eng))
+                if rc:
+                    raise RuntimeError(f"tf_host_engine_create: {L.tf_strerror(rc).decode()} "
+                                       f"({L.tf_last_cuda_error().decode()})")
                 _engines[key] = eng
     return eng

@@ -218,6 +218,29 @@ int ensure_scratch(HostEngine* g, size_t pb, int64_t cnt) {
   return TF_OK;
 }
 
+// An explicit leaf larger than a staging slot (leaf_log2 up to 24): grow the
+// slots so a chunk always holds at least one whole leaf.
+int grow_slots(HostEngine* g, size_t bytes) {
+  if (bytes <= g->chunk) return TF_OK;
+  int rc;
+  if ((rc = cu(cudaStreamSynchronize(g->cstream)))) return rc;
+  if ((rc = cu(cudaStreamSynchronize(g->stream)))) return rc;
+  bytes = (bytes + 4095) & ~size_t(4095);
+  for (int b = 0; b < 2; ++b) {
+    cudaFreeHost(g->pin[b]);
+    cudaFree(g->dev[b]);
+    g->pin[b] = nullptr;
+    g->dev[b] = nullptr;
+  }
+  g->chunk = 0;
+  for (int b = 0; b < 2; ++b) {
+    if ((rc = cu(cudaHostAlloc(reinterpret_cast<void**>(&g->pin[b]), 2 * bytes, cudaHostAllocDefault)))) return rc;
+    if ((rc = cu(cudaMalloc(reinterpret_cast<void**>(&g->dev[b]), 2 * bytes)))) return rc;
+  }
+  g->chunk = bytes;
+  return TF_OK;
+}
+
 constexpr size_t kPiece = size_t(2) << 20;
 
 // Stage `bytes` of operand k (0 = x, 1 = y) from host `src` into device slot b.
@@ -342,6 +365,7 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
     return TF_EINVAL_ARG;  // mixed host/device operands
   } else {
     const int64_t L = int64_t(1) << lg;
+    if ((rc = tfb::grow_slots(g, static_cast<size_t>(std::min<int64_t>(L, n)) * item))) return rc;
     const int64_t chunk_leaves = std::max<int64_t>(1, static_cast<int64_t>(g->chunk / (L * item)));
     const int64_t chunk_elems = chunk_leaves * L;
     const auto* cx = static_cast<const char*>(hx);

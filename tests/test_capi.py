@@ -87,3 +87,17 @@ def test_host_engine_entry_points_without_gpu(lib):
         assert lib.tf_host_engine_destroy(eng) == _lib.TF_OK
     else:
         assert rc in (_lib.TF_ECUDA, _lib.TF_EINVAL_ARG) and not eng.value
+
+
+def test_first_host_engine_call_loads_the_library_without_deadlock():
+    """host_engine() as the very first library call (lib() not loaded yet) must not
+    self-deadlock on the loader lock; with no GPU it raises instead."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_1401_0248_b200 import _lib\n"
+            "try:\n    _lib.host_engine(0)\n    print('created')\n"
+            "except RuntimeError as e:\n    print('raised', e)\n") % REPO
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.startswith(("created", "raised"))

@@ -225,6 +225,10 @@ def test_streamed_host_path_equals_device_path(tfb, oracle, cuda):
     _same((r.value, r.error), oracle.emulate(2, xh, yh), "wrapper")
     got = tfb.reduce(tfb.Method.KAHAN, torch.from_numpy(xh)).cpu().numpy()
     _same(got, oracle.emulate(4, xh), "reduce host")
+    # an explicit leaf (2^21 f64 = 16 MiB) larger than the 1 MiB staging slots: slots grow
+    got = api._host_pair(tfb.Method.TWOFOLD_RIGOROUS, torch.from_numpy(xh), torch.from_numpy(yh), dev,
+                         leaf_log2=21, engine=eng)
+    _same(got, oracle.emulate(3, xh, yh, 21), "leaf larger than a slot")
     with pytest.raises(ValueError):  # mixed host/device operands are refused by the engine
         lib = _lib.lib()
         p = np.empty(2)
