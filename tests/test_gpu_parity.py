@@ -676,3 +676,18 @@ def test_non_finite_inputs_grid_and_seq(tfb, oracle, cuda):
                         if n <= 5_001:
                             seq = tfb.reduce(meth, xd, yy, flavor=tfb.Flavor.sequential()).cpu().numpy()
                             _same_nf(seq, oracle.seq(m, x, yyh), (dt, n, pat, m, dot, "seq"))
+
+
+def test_wrappers_accept_strided_numpy_lists_and_views(tfb, oracle, cuda):
+    """kernels.py:575 copies non-contiguous inputs (np.ascontiguousarray): strided
+    numpy views, Python lists and CPU tensors give the contiguous array's result."""
+    base = oracle.lcg_fill("mmix", 20_002, 111, np.float64, True)
+    view = base[::2]
+    want = oracle.emulate(2, np.ascontiguousarray(view))
+    for arg in (view, list(view), torch.from_numpy(base)[::2]):
+        r = tfb.sum_twofold_fast(arg)
+        assert _hex(r.value) == _hex(want[0]) and _hex(r.error) == _hex(want[1]), type(arg)
+    f32 = base.astype(np.float32)
+    r = tfb.sum_wide(f32[1::3])
+    w = oracle.emulate(1, np.ascontiguousarray(f32[1::3]))
+    assert _hex(r.value) == _hex(w[0]) and type(r.value) is np.float64
