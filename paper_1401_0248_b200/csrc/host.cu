@@ -3,7 +3,8 @@
 // on host memory, as one native call.
 //
 // An engine owns, per device: a non-blocking stream, two staging slots (pinned
-// host + device, `chunk` bytes per operand each), grow-on-demand leaf partials
+// host + device, up to `chunk` bytes per operand each, allocated at 1 MiB and
+// grown on the first larger input), grow-on-demand leaf partials
 // and retire counters, a pinned result pair, and a small memcpy thread pool.
 //
 // tf_host_reduce(engine, method, dtype, hx, hy, n, leaf_log2, out_pair_host):
@@ -152,7 +153,8 @@ Mem classify(const void* p, int device) {
 
 struct HostEngine {
   int device = 0;
-  size_t chunk = 0;  // bytes per operand per slot
+  size_t chunk = 0;         // bytes per operand per slot, as allocated
+  size_t chunk_target = 0;  // slot size large inputs grow to (creation argument)
   cudaStream_t stream = nullptr;   // kernels (and all work of single-chunk calls)
   cudaStream_t cstream = nullptr;  // H2D copies of multi-chunk calls
   char* pin[2] = {nullptr, nullptr};  // [x | y] per slot
@@ -218,8 +220,8 @@ int ensure_scratch(HostEngine* g, size_t pb, int64_t cnt) {
   return TF_OK;
 }
 
-// An explicit leaf larger than a staging slot (leaf_log2 up to 24): grow the
-// slots so a chunk always holds at least one whole leaf.
+// Grow the staging slots (first large input, or an explicit leaf larger than a
+// slot — leaf_log2 up to 24 — so that a chunk always holds one whole leaf).
 int grow_slots(HostEngine* g, size_t bytes) {
   if (bytes <= g->chunk) return TF_OK;
   int rc;
@@ -286,7 +288,10 @@ int tf_host_engine_create(int device, int threads, size_t chunk_bytes, void** en
   tfb::DeviceGuard guard(device);
   auto* g = new HostEngine();
   g->device = device;
-  g->chunk = chunk_bytes;
+  // Slots start at 1 MiB (fast creation, small calls never pay for more) and grow
+  // to chunk_bytes the first time a larger input arrives.
+  g->chunk_target = chunk_bytes;
+  g->chunk = std::min(chunk_bytes, size_t(1) << 20);
   int rc = TF_OK;
   auto step = [&](cudaError_t e) {
     if (rc == TF_OK) rc = tfb::cu(e);
@@ -294,8 +299,8 @@ int tf_host_engine_create(int device, int threads, size_t chunk_bytes, void** en
   step(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
   step(cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking));
   for (int b = 0; b < 2 && rc == TF_OK; ++b) {
-    step(cudaHostAlloc(reinterpret_cast<void**>(&g->pin[b]), 2 * chunk_bytes, cudaHostAllocDefault));
-    step(cudaMalloc(reinterpret_cast<void**>(&g->dev[b]), 2 * chunk_bytes));
+    step(cudaHostAlloc(reinterpret_cast<void**>(&g->pin[b]), 2 * g->chunk, cudaHostAllocDefault));
+    step(cudaMalloc(reinterpret_cast<void**>(&g->dev[b]), 2 * g->chunk));
     step(cudaEventCreateWithFlags(&g->h2d_done[b], cudaEventDisableTiming));
     step(cudaEventCreateWithFlags(&g->k_done[b], cudaEventDisableTiming));
   }
@@ -365,7 +370,10 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
     return TF_EINVAL_ARG;  // mixed host/device operands
   } else {
     const int64_t L = int64_t(1) << lg;
-    if ((rc = tfb::grow_slots(g, static_cast<size_t>(std::min<int64_t>(L, n)) * item))) return rc;
+    // slot size for this call: the whole input up to the target, never less than one leaf
+    const size_t want = std::max(std::min(static_cast<size_t>(n) * item, g->chunk_target),
+                                 static_cast<size_t>(std::min<int64_t>(L, n)) * item);
+    if ((rc = tfb::grow_slots(g, want))) return rc;
     const int64_t chunk_leaves = std::max<int64_t>(1, static_cast<int64_t>(g->chunk / (L * item)));
     const int64_t chunk_elems = chunk_leaves * L;
     const auto* cx = static_cast<const char*>(hx);
