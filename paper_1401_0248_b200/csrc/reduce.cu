@@ -10,11 +10,16 @@
 //   leaf pair balanced contiguous binary tree over the 256 thread states
 //             (warp shuffles, then one shared-memory level)
 //   row pair  balanced contiguous binary tree over the row's leaf pairs,
-//             padded with (+0,+0) to a power of two, done by the CTA that
-//             retires the row's last leaf (atomic ticket; merge order is by
-//             leaf index, never by arrival order)
+//             padded with (+0,+0) to a power of two (merge order by leaf
+//             index, never by arrival order), built by one of three tails:
+//             the CTA that retires the row's last leaf (atomic ticket; the
+//             TMA loader), a programmatic-dependent tree kernel (the LDG
+//             loader's default), or — inputs of <= 64 one-vector leaves — one
+//             thread-block cluster merging through DSMEM (small.cuh)
 // The partition depends only on (dtype, n, leaf_log2), so results are
-// bit-identical across reruns, grid sizes and SM counts.
+// bit-identical across reruns, grid sizes, tails, loaders and SM counts.
+// Loaders: 128-bit LDG streaming (here) or the warp-specialised bulk-copy
+// pipeline (tma.cuh), chosen per size from the measured loader_table.inc.
 #include <cuda_runtime.h>
 
 #include <cstdint>
