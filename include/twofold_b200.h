@@ -268,9 +268,9 @@ int tf_host_engine_threads(const void* engine);
  * elements, host memory); blocks until done.  Pageable inputs go through the
  * pinned slots (the pool copies chunk c+1 while chunk c is on the DMA engine
  * and its leaves reduce); page-locked inputs DMA directly; device pointers (of
- * the engine's device) reduce in place.  after_stream (may be NULL): the
- * stream device / page-locked operands are ordered on — the engine's work
- * starts after that stream's pending work.  Leaf-aligned chunks: bit-identical
+ * the engine's device) reduce in place.  after_stream: the stream device /
+ * page-locked operands are ordered on (NULL = the legacy default stream) —
+ * the engine's work starts after that stream's pending work.  Leaf-aligned chunks: bit-identical
  * to tf_reduce.  Calls on one engine are serialised. */
 int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const void* hy, int64_t n,
                    int leaf_log2, void* out_pair_host, void* after_stream);

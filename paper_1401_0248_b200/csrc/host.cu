@@ -357,8 +357,8 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
   const tfb::Mem ky = dot && n > 0 ? tfb::classify(hy, g->device) : kx;
   if (kx == tfb::Mem::kOtherDevice || ky == tfb::Mem::kOtherDevice) return TF_EINVAL_ARG;
   // Device or page-locked operands may still be in flight on the caller's
-  // stream: order the engine's streams after it.
-  if (after_stream && (kx != tfb::Mem::kPageable || ky != tfb::Mem::kPageable)) {
+  // stream (NULL = the legacy default stream): order the engine's streams after it.
+  if (kx != tfb::Mem::kPageable || ky != tfb::Mem::kPageable) {
     if ((rc = tfb::cu(cudaEventRecord(g->entry, static_cast<cudaStream_t>(after_stream))))) return rc;
     if ((rc = tfb::cu(cudaStreamWaitEvent(g->stream, g->entry, 0)))) return rc;
     if ((rc = tfb::cu(cudaStreamWaitEvent(g->cstream, g->entry, 0)))) return rc;
