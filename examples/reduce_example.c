@@ -1,6 +1,8 @@
 /* Native caller of the C ABI (include/twofold_b200.h): generate cfg5-like data on
  * the device, run the twofold dot through tf_reduce on a user stream, print the
- * (value, error) pair and the exact sum from tf_exact.
+ * (value, error) pair and the exact sum from tf_exact; then reduce the same data
+ * from plain malloc'd host arrays through the host-buffer engine
+ * (tf_host_reduce) and check the pair is bit-identical.
  *
  *   cc reduce_example.c -I../include -I/usr/local/cuda/include \
  *      -L../paper_1401_0248_b200 -ltwofold_b200 -L/usr/local/cuda/lib64 -lcudart \
@@ -53,5 +55,23 @@ int main(int argc, char** argv) {
   printf("launch: %s\n", tf_last_launch());
   /* v + e must equal the exact sum to well below one ulp of it */
   const double dev = (h[0] - e[0]) + (h[1] - e[1]);
-  return (dev < 0 ? -dev : dev) <= 1e-13 * (e[0] < 0 ? -e[0] : e[0]) + 1e-300 ? 0 : 2;
+  if ((dev < 0 ? -dev : dev) > 1e-13 * (e[0] < 0 ? -e[0] : e[0]) + 1e-300) return 2;
+
+  /* the same dot from pageable host memory: one blocking call */
+  double* hx = (double*)malloc(n * sizeof(double));
+  double* hy = (double*)malloc(n * sizeof(double));
+  if (!hx || !hy) return 1;
+  if (cudaMemcpy(hx, x, n * sizeof(double), cudaMemcpyDeviceToHost) ||
+      cudaMemcpy(hy, y, n * sizeof(double), cudaMemcpyDeviceToHost))
+    return 1;
+  void* engine = NULL;
+  double hp[2];
+  CK(tf_host_engine_create(0, 0, 0, &engine));
+  CK(tf_host_reduce(engine, TF_TWOFOLD_FAST, TF_F64, hx, hy, n, 0, hp, NULL));
+  printf("host engine (%d copy threads): value=%.17g error=%.17g %s\n", tf_host_engine_threads(engine), hp[0],
+         hp[1], (hp[0] == h[0] && hp[1] == h[1]) ? "bit-identical" : "MISMATCH");
+  CK(tf_host_engine_destroy(engine));
+  free(hx);
+  free(hy);
+  return (hp[0] == h[0] && hp[1] == h[1]) ? 0 : 3;
 }

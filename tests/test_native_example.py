@@ -33,4 +33,4 @@ def test_native_example_runs(tmp_path, cuda):
     exe = _build(tmp_path)
     out = subprocess.run([exe, str(1 << 22)], capture_output=True, text=True, timeout=120)
     assert out.returncode == 0, out.stdout + out.stderr
-    assert "value=" in out.stdout and "leaves_" in out.stdout
+    assert "value=" in out.stdout and "leaves_" in out.stdout and "bit-identical" in out.stdout
