@@ -48,6 +48,7 @@ __global__ void __launch_bounds__(kThreads) small_cluster_kernel(const T* __rest
   cg::cluster_group cluster = cg::this_cluster();
   const int c = static_cast<int>(cluster.block_rank());
   const int C = static_cast<int>(cluster.num_blocks());
+  TFB_CHECK(C <= kSmallMaxCluster && int64_t(C) * G >= P && gridDim.x == static_cast<unsigned>(C));
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int gsz = static_cast<int>(P2 < G ? P2 : G);  // leaves of this CTA's subtree
 
@@ -59,6 +60,7 @@ __global__ void __launch_bounds__(kThreads) small_cluster_kernel(const T* __rest
     const int64_t start = (int64_t(c) * G + g) * Lel;
     full[g] = VEC && g < gsz && start + Lel <= n;
     if (full[g]) {
+      TFB_CHECK((reinterpret_cast<uintptr_t>(x + start) & 15u) == 0 && start + Lel <= n);
       a[g] = ld_stream(reinterpret_cast<const VT*>(x + start) + t);
       if constexpr (DOT) b[g] = ld_stream(reinterpret_cast<const VT*>(y + start) + t);
     }
