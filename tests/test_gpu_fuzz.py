@@ -71,3 +71,31 @@ def test_small_instance_criterion_c6_on_the_grid(tfb, oracle):
         n = int(rng.integers(1, 21))
         data = (rng.uniform(-1, 1, n) * 2.0 ** rng.integers(-8, 8, n))
         check(data.astype(np.float32), 2.0 ** -24)
+
+
+def test_every_loader_every_chain_length(tfb, oracle, cuda):
+    """Systematic: every loader (LDG, LDG deep, four TMA ring shapes) x precision x
+    sum/dot x method x leaf size from one vector per chain (R = 1) up to R = 32 —
+    in particular R below the loader's batch depth U — bit-identical to the emulator."""
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    rng = np.random.default_rng(77)
+    try:
+        for dt in (np.float32, np.float64):
+            floor = 10 if dt == np.float32 else 9
+            for lg in range(floor, floor + 6):
+                n = (1 << lg) * 37 + int(rng.integers(1, 1 << lg))
+                xh = (rng.standard_normal(n) * 2.0 ** rng.integers(-6, 6, n)).astype(dt)
+                yh = rng.uniform(-1, 1, n).astype(dt)
+                x, y = torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda)
+                for m in ((0, 2, 3, 4) if dt == np.float64 else (0, 1, 2, 3, 4)):
+                    meth = list(tfb.Method)[m]
+                    for dot in (False, True):
+                        want = oracle.emulate(m, xh, yh if dot else None, lg)
+                        for loader in (1, 8, 2, 3, 6, 7):
+                            L.tf_set_loader(loader)
+                            got = tfb.reduce(meth, x, y if dot else None, leaf_log2=lg).cpu().numpy()
+                            assert float(got[0]).hex() == float(want[0]).hex() and \
+                                float(got[1]).hex() == float(want[1]).hex(), (dt, lg, m, dot, loader, got, want)
+    finally:
+        L.tf_set_loader(0)
