@@ -42,6 +42,16 @@ def main():
     ref = tfb.sharded_reduce(tfb.Method.TWOFOLD_RIGOROUS, x, y, n_global=n_global, force_collective=True,
                              track_product=True).cpu()
     assert torch.equal(got, ref)
+    # the TMA loader finishes the combine inside its own single launch: force it
+    from paper_1401_0248_b200 import _lib
+    for loader in (2, 3, 6, 7):
+        _lib.lib().tf_set_loader(loader)
+        got = tfb.sharded_reduce(tfb.Method.TWOFOLD_FAST, x, y, n_global=n_global, combine="peer").cpu()
+        ref = tfb.sharded_reduce(tfb.Method.TWOFOLD_FAST, x, y, n_global=n_global, combine="nccl",
+                                 force_collective=True).cpu()
+        assert torch.equal(got, ref), (loader, got, ref)
+        checked += 1
+    _lib.lib().tf_set_loader(0)
     assert not tdist.peer_combine_error()
     # combine="auto": the one-time self-check (peer vs NCCL on known data) passes on every rank
     for acc in (torch.float32, torch.float64):
