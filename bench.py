@@ -42,6 +42,9 @@ PER_RANK = 1 << 29
 WORKLOADS = {
     # name: (config key, method, per-rank elements or None = whole config, needs L2 flush)
     "cfg5": ("cfg5", "twofold-fast", PER_RANK, False),
+    # cfg5 exactly as BASELINE.json states it: N = 2^32 fixed, split over the ranks
+    # (strong scaling; at N=1 the whole 2 x 32 GiB on one GPU)
+    "cfg5-full": ("cfg5", "twofold-fast", "strong", False),
     "cfg1": ("cfg1", "twofold-fast", None, True),
     "cfg2": ("cfg2", "twofold-fast", None, True),
     "cfg2-dott": ("cfg2", "twofold-rigorous", None, True),
@@ -94,7 +97,8 @@ def workload_desc(name, cfg, method, n_rank, world):
     d = {
         "workload": (f"{name}: {cfg.note}; {method} on {n_rank} elements per rank"
                      + (f" (rank r owns [r*2^29,(r+1)*2^29) of the 2^32 stream; N=8 is cfg5 in full)"
-                        if name == "cfg5" else "")),
+                        if name == "cfg5" else "")
+                     + (f" (the full 2^32 stream split evenly over {world} rank(s))" if name == "cfg5-full" else "")),
         "op": cfg.op, "method": method, "n_per_rank": n_rank, "n_global": n_rank * world,
         "data_dtype": "f64" if str(cfg.dtype).endswith("64") else "f32",
         "generator": f"Philox4x32-10 seed {cfg.seed} (x stream 0, y stream 1)",
@@ -198,6 +202,8 @@ def run_reference(args):
     import torch  # noqa: F401  (only for dtype names in the config)
     from paper_1401_0248_b200.gen import CONFIGS
     cfg = CONFIGS[cfg_key]
+    if n_rank == "strong":
+        n_rank = cfg.n // world
     mid = O.METHODS.index(method)
     nt = host_threads()
     dt = np.float64 if str(cfg.dtype).endswith("64") else np.float32
@@ -227,7 +233,8 @@ def run_reference(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64" if dt == np.float64 else "f32",
+        "scaling": "strong" if WORKLOADS[args.config][2] == "strong" else "weak", "vs_baseline": None,
+        "dtype": "f64" if dt == np.float64 else "f32",
         "data": "synthetic", "impl": "reference",
         "config": workload_desc(args.config, cfg, method, n, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": nt, "kind": "port",
@@ -260,6 +267,9 @@ def run_ours(args):
 
     cfg_key, method_name, n_rank, flush = WORKLOADS[args.config]
     cfg = CONFIGS[cfg_key]
+    strong = n_rank == "strong"
+    if strong:
+        n_rank = cfg.n // world
     method = tfb.Method(method_name)
     rows = cfg.op == "rows-dot"
     n = n_rank or cfg.n
@@ -481,7 +491,8 @@ def run_ours(args):
     dtype_name = "f64" if item == 8 else "f32"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong" if strong else "weak",
+        "vs_baseline": None,
         "dtype": dtype_name, "data": "synthetic",
         "config": dict(workload_desc(args.config, cfg, method_name, n, world),
                        l2=(f"rotating over {R} input copies ({R * bytes_per_step / 1e6:.0f} MB >= 4x the 126 MB L2)"
