@@ -1,5 +1,9 @@
 """Tail variants on the LDG path: auto (PDL) vs ticket vs cluster-group tail (tail 3),
-graph-replayed over rotating copies (>= 4x L2); every variant checked bit-identical."""
+graph-replayed over rotating copies (>= 4x L2); every variant checked bit-identical.
+
+Record of a rejected experiment (profiles/r01_summary.md): the cluster-group tail
+(tail 3) was removed from the library after this measurement; tf_set_tail(3) now
+fails and the T3 columns repeat the automatic tail."""
 import os
 import sys
 
