@@ -202,8 +202,8 @@ def run_reference(args):
     import torch  # noqa: F401  (only for dtype names in the config)
     from paper_1401_0248_b200.gen import CONFIGS
     cfg = CONFIGS[cfg_key]
-    if n_rank == "strong":
-        n_rank = cfg.n // world
+    if n_rank == "strong":  # bounded sample: the rank-0 slice, at most one 2^29 shard
+        n_rank = min(cfg.n // world, PER_RANK)
     mid = O.METHODS.index(method)
     nt = host_threads()
     dt = np.float64 if str(cfg.dtype).endswith("64") else np.float32
