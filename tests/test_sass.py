@@ -35,7 +35,8 @@ def sass():
     return funcs
 
 
-REDUCTION = ("leaves_kernel", "leaves_tma_kernel", "tree_kernel", "rows_tree_kernel", "seq_kernel", "lanes_kernel",
+REDUCTION = ("leaves_kernel", "leaves_tma_kernel", "small_cluster_kernel", "tree_kernel", "rows_tree_kernel", "seq_kernel",
+             "lanes_kernel",
              "canary_kernel", "eft_kernel", "noread_kernel")
 
 
