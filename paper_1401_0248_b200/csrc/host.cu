@@ -20,7 +20,9 @@
 //     copy and DMA straight from the caller's memory; device pointers skip the
 //     copies altogether.
 //   * pageable staging is pipelined in 2 MiB pieces (the DMA of piece i
-//     overlaps the pool's copy of piece i+1).
+//     overlaps the pool's copy of piece i+1);
+//   * small inputs (<= 128 KiB pageable / 256 KiB page-locked per operand)
+//     skip the DMA: the kernel reads them over PCIe from page-locked memory.
 // Calls on one engine are serialised by its mutex; the call blocks until the
 // pair is in out_pair_host.
 #include <cuda_runtime.h>
@@ -244,6 +246,13 @@ int grow_slots(HostEngine* g, size_t bytes) {
 }
 
 constexpr size_t kPiece = size_t(2) << 20;
+// Inputs up to this size per operand are read by the kernel in place from
+// page-locked host memory (zero-copy) instead of being DMA'd first.  Pageable
+// inputs must be copied into the staging slot first, which the DMA path
+// overlaps with the transfer, hence the lower bound (measured crossovers,
+// scripts/tiny_latency.py and scripts/host_engine_probe.py).
+constexpr size_t kZeroCopyMaxPinned = size_t(256) << 10;
+constexpr size_t kZeroCopyMaxPageable = size_t(128) << 10;
 
 // Stage `bytes` of operand k (0 = x, 1 = y) from host `src` into device slot b.
 int stage(HostEngine* g, cudaStream_t s, int b, int k, const char* src, size_t bytes, Mem kind, bool wait_slot) {
@@ -378,6 +387,42 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
     const int64_t chunk_elems = chunk_leaves * L;
     const auto* cx = static_cast<const char*>(hx);
     const auto* cy = static_cast<const char*>(hy);
+    const size_t bytes_all = static_cast<size_t>(n) * item;
+    const bool pageable = kx == tfb::Mem::kPageable || (dot && ky == tfb::Mem::kPageable);
+    if (n > 0 && bytes_all <= (pageable ? tfb::kZeroCopyMaxPageable : tfb::kZeroCopyMaxPinned)) {
+      // Small input: no DMA at all.  The kernel reads the operands over PCIe
+      // straight from page-locked host memory (the staging slot, or the caller's
+      // own pinned buffer); one launch, one sync.
+      const void* dx = hx;
+      const void* dy = hy;
+      if (kx == tfb::Mem::kPageable) {
+        std::memcpy(g->pin[0], cx, bytes_all);
+        dx = g->pin[0];
+      } else if (cudaHostGetDevicePointer(const_cast<void**>(&dx), const_cast<void*>(hx), 0) != cudaSuccess) {
+        cudaGetLastError();
+        dx = nullptr;
+      }
+      if (dot) {
+        if (ky == tfb::Mem::kPageable) {
+          std::memcpy(g->pin[0] + g->chunk, cy, bytes_all);
+          dy = g->pin[0] + g->chunk;
+        } else if (cudaHostGetDevicePointer(const_cast<void**>(&dy), const_cast<void*>(hy), 0) != cudaSuccess) {
+          cudaGetLastError();
+          dy = nullptr;
+        }
+      }
+      if (dx && (!dot || dy)) {
+        rc = tf_reduce(method, dtype, dx, dot ? dy : nullptr, n, lg, g->pair_pin, g->partials, g->partials_bytes,
+                       g->counters, g->counters_len, g->stream);
+        if (rc) {
+          cudaStreamSynchronize(g->stream);
+          return rc;
+        }
+        if ((rc = tfb::cu(cudaStreamSynchronize(g->stream)))) return rc;
+        std::memcpy(out_pair_host, g->pair_pin, pair_bytes);
+        return TF_OK;
+      }
+    }
     if (n <= chunk_elems) {
       const size_t bytes = n * item;
       if (n > 0) {

@@ -218,6 +218,13 @@ def test_streamed_host_path_equals_device_path(tfb, oracle, cuda):
             _same(got, oracle.emulate(m, xh), (m, pinned, "sum"))
         got = api._host_pair(tfb.Method.TWOFOLD_FAST, xt[:0], None, dev, engine=eng)
         assert got.tolist() == [0.0, 0.0]
+        # small inputs take the zero-copy path (kernel reads page-locked host memory):
+        # whole buffers and interior slices of them
+        for a, b in ((0, 4097), (3, 9000), (1000, 1000 + (1 << 15))):
+            for m in (2, 3):
+                meth = list(tfb.Method)[m]
+                got = api._host_pair(meth, xt[a:b], yt[a:b], dev, engine=eng)
+                _same(got, oracle.emulate(m, xh[a:b], yh[a:b]), (m, pinned, a, b, "zero-copy"))
     xf = xh.astype(np.float32)
     got = api._host_pair(tfb.Method.WIDE, torch.from_numpy(xf), None, dev, engine=eng)
     _same(got, oracle.emulate(1, xf), "wide")
