@@ -464,17 +464,38 @@ def _run_numpy(method: Method, a: np.ndarray, b: np.ndarray | None, track_produc
         a = np.ascontiguousarray(a)
     if b is not None and not b.flags.c_contiguous:
         b = np.ascontiguousarray(b)
-    if not torch.cuda.is_available():
-        raise RuntimeError("no CUDA device available: the twofold B200 library has no CPU path")
+    global _cuda_seen
+    if not _cuda_seen:
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device available: the twofold B200 library has no CPU path")
+        _cuda_seen = True
     dev = torch.cuda.current_device()
     _lib.ensure_canary(dev)
-    pair = np.empty(2, dtype=np.float64 if method is Method.WIDE else a.dtype)
-    check(lib().tf_host_reduce(_lib.host_engine(dev), mid, code, a.ctypes.data,
-                               None if b is None else b.ctypes.data, a.shape[0], 0, pair.ctypes.data, None),
-          "tf_host_reduce")
+    pair, pair_ptr = _pair_buffer(np.float64 if method is Method.WIDE else a.dtype)
+    rc = lib().tf_host_reduce(_lib.host_engine(dev), mid, code, a.__array_interface__["data"][0],
+                              None if b is None else b.__array_interface__["data"][0], a.shape[0], 0, pair_ptr,
+                              None)
+    if rc:
+        check(rc, "tf_host_reduce")
     if method in _TWOFOLD_METHODS:
-        return SumResult(Twofold(pair[0], pair[1]), a.shape[0])
+        return SumResult(Twofold(pair[0], pair[1]), a.shape[0])  # numpy scalars: copies, the buffer is reused
     return SumResult(Twofold(pair[0], pair.dtype.type(0)), a.shape[0])
+
+
+_cuda_seen = False
+_pair_tls = threading.local()
+
+
+def _pair_buffer(dtype) -> tuple[np.ndarray, int]:
+    """A per-thread 2-element result buffer and its address (one per dtype)."""
+    cache = getattr(_pair_tls, "bufs", None)
+    if cache is None:
+        cache = _pair_tls.bufs = {}
+    rec = cache.get(dtype)
+    if rec is None:
+        buf = np.empty(2, dtype=dtype)
+        rec = cache[dtype] = (buf, buf.ctypes.data)
+    return rec
 
 
 def raw_sum_kernel(method: Method, flavor: Flavor, dtype):
