@@ -247,9 +247,15 @@ def sharded_reduce(method: Method, x_local: torch.Tensor, y_local: torch.Tensor 
     _, world = _world(group)
     if world == 1 and not (force_collective and dist.is_available() and dist.is_initialized()):
         return local  # force_collective exercises the all-gather + merge path at world size 1
-    parts = [torch.empty_like(local) for _ in range(world)]
-    dist.all_gather(parts, local.contiguous(), group=group)
-    gathered = torch.stack(parts, 0)
+    local = local.contiguous()
+    if local.is_cuda and dist.get_backend(group) == "nccl":
+        # one NCCL all-gather straight into the (world, 2) pair table
+        gathered = torch.empty((world, 2), dtype=local.dtype, device=local.device)
+        dist.all_gather_into_tensor(gathered, local, group=group)
+    else:
+        parts = [torch.empty_like(local) for _ in range(world)]
+        dist.all_gather(parts, local, group=group)
+        gathered = torch.stack(parts, 0)
     return (merge or _default_merge)(method, gathered)
 
 
