@@ -451,9 +451,13 @@ def run_ours(args):
         e2e = {"value": n * world * ke / wall / 1e9, "unit": UNIT, "h2d_bytes_per_step": bytes_per_step,
                "d2h_bytes_per_step": 16 if not rows else cfg.rows * item,
                "steps": ke, "ms_per_step": 1e3 * wall / ke,
-               "path": ("paper_1401_0248_b200.sharded_run(pinned host shard) -> C-ABI tf_host_reduce (host-buffer "
-                        "engine): leaf-aligned 16 MiB chunks DMA'd straight from the pinned shard on a copy stream, "
-                        "overlapped with the leaf kernels; tree kernel stores the pair into mapped host memory"),
+               "path": (("paper_1401_0248_b200.dot_rows(pinned host matrices) -> C-ABI tf_host_reduce_rows "
+                         "(host-buffer engine): 16 MiB row blocks DMA'd straight from the pinned matrices on a copy "
+                         "stream, overlapped with the row kernels; row pairs stored into mapped host memory")
+                        if rows else
+                        ("paper_1401_0248_b200.sharded_run(pinned host shard) -> C-ABI tf_host_reduce (host-buffer "
+                         "engine): leaf-aligned 16 MiB chunks DMA'd straight from the pinned shard on a copy stream, "
+                         "overlapped with the leaf kernels; tree kernel stores the pair into mapped host memory")),
                "timing": "wall clock around the steps after synchronize, max over ranks"}
         # The link the e2e path streams over: plain pinned H2D of the same host
         # buffer (up to 1 GiB, best of 3, CUDA events) — the e2e ceiling.

@@ -275,6 +275,16 @@ int tf_host_engine_threads(const void* engine);
 int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const void* hy, int64_t n,
                    int leaf_log2, void* out_pair_host, void* after_stream);
 
+/* Row-wise form (tf_reduce_rows on host matrices): rows x cols with leading
+ * dimensions ldx / ldy (elements); out_pairs_host: rows (value, error) pairs.
+ * Row blocks are packed into the staging slots (pitched DMA for page-locked
+ * strided input) and reduced while the next block is in flight; the leaf size
+ * is the whole matrix's, so every row is bit-identical to tf_reduce_rows on
+ * the same matrix.  rows == 1 is the 1-D call. */
+int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, const void* hy, int64_t rows,
+                        int64_t cols, int64_t ldx, int64_t ldy, int leaf_log2, void* out_pairs_host,
+                        void* after_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,7 @@ def _bind(L):
         "tf_host_engine_destroy": ([vp], i32),
         "tf_host_engine_threads": ([vp], i32),
         "tf_host_reduce": ([vp, i32, i32, vp, vp, i64, i32, vp, vp], i32),
+        "tf_host_reduce_rows": ([vp, i32, i32, vp, vp, i64, i64, i64, i64, i32, vp, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

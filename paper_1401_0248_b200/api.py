@@ -584,6 +584,16 @@ def reduce_rows(method: Method, X, Y=None, *, leaf_log2: int = 0,
     mid = _mid(method, track_product, y is not None)
     dev = _device_for(x)
     with torch.cuda.device(dev):
+        if _all_host(x, y):  # host matrices: the host-buffer engine, row blocks overlapped
+            _lib.ensure_canary(dev.index)
+            rows, cols = x.shape
+            pairs = np.empty((rows, 2), dtype=_np_type(_acc_dtype(method, x.dtype)))
+            check(lib().tf_host_reduce_rows(_lib.host_engine(dev.index), mid, _dtype_code(x.dtype), x.data_ptr(),
+                                            _ptr(y), rows, cols, x.stride(0), 0 if y is None else y.stride(0),
+                                            leaf_log2, pairs.ctypes.data, _stream_ptr(dev)), "tf_host_reduce_rows")
+            if out is None:
+                return torch.from_numpy(pairs).to(dev)
+            return out.copy_(torch.from_numpy(pairs))
         if not x.is_cuda:
             x = x.to(dev, non_blocking=x.is_pinned())
         if y is not None and not y.is_cuda:

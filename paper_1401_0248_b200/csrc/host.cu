@@ -165,6 +165,8 @@ struct HostEngine {
   cudaEvent_t k_done[2] = {nullptr, nullptr};    // slot's leaf kernel finished (device slot reusable)
   cudaEvent_t entry = nullptr;                   // the caller's stream at entry (device / pinned inputs)
   void* pair_pin = nullptr;  // mapped pinned: the last kernel stores the pair straight into it
+  void* rows_pin = nullptr;  // mapped pinned row pairs (rows family), grown on demand
+  size_t rows_pin_bytes = 0;
   void* partials = nullptr;
   size_t partials_bytes = 0;
   void* counters = nullptr;
@@ -190,6 +192,7 @@ void release(HostEngine* g) {
     if (g->k_done[b]) cudaEventDestroy(g->k_done[b]);
   }
   if (g->pair_pin) cudaFreeHost(g->pair_pin);
+  if (g->rows_pin) cudaFreeHost(g->rows_pin);
   if (g->partials) cudaFree(g->partials);
   if (g->counters) cudaFree(g->counters);
   if (g->entry) cudaEventDestroy(g->entry);
@@ -462,6 +465,105 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
   }
   if ((rc = tfb::cu(cudaStreamSynchronize(g->stream)))) return rc;
   std::memcpy(out_pair_host, g->pair_pin, pair_bytes);
+  return TF_OK;
+}
+
+int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, const void* hy, int64_t rows,
+                        int64_t cols, int64_t ldx, int64_t ldy, int leaf_log2, void* out_pairs_host,
+                        void* after_stream) {
+  if (!engine || (!out_pairs_host && rows > 0)) return TF_EINVAL_ARG;
+  if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
+  if (rows < 0 || cols < 0) return TF_EINVAL_SHAPE;
+  if (rows > 1 && (ldx < cols || (hy && ldy < cols))) return TF_EINVAL_SHAPE;
+  if (rows == 1)  // one row is the 1-D reduction (chunked within the row)
+    return tf_host_reduce(engine, method, dtype, hx, hy, cols, leaf_log2, out_pairs_host, after_stream);
+  if (rows == 0) return TF_OK;
+  if (cols > 0 && !hx) return TF_EINVAL_ARG;
+  auto* g = static_cast<HostEngine*>(engine);
+  std::lock_guard<std::mutex> lk(g->mu);
+  tfb::DeviceGuard guard(g->device);
+  const int base = method & ~TF_TRACK_PRODUCT;
+  const size_t pair_bytes = (base == TF_WIDE ? 8 : (dtype == TF_F64 ? 8 : 4)) * 2;
+  const size_t item = dtype == TF_F64 ? 8 : 4;
+  const bool dot = hy != nullptr;
+  // the leaf size is the WHOLE matrix's (tf_reduce_rows resolves it from rows * cols),
+  // so every row block reduces exactly as the single-launch call would
+  int rc;
+  size_t pb = 0;
+  int64_t cnt = 0, leaves = 0;
+  if ((rc = tf_workspace_size(method, dtype, rows, cols, leaf_log2, &pb, &cnt, &leaves))) return rc;
+  const int lg = leaf_log2 ? leaf_log2 : tf_leaf_log2(dtype, rows * cols);
+  if ((rc = tfb::ensure_scratch(g, std::max<size_t>(pb, pair_bytes), std::max<int64_t>(cnt, 1)))) return rc;
+  if (static_cast<size_t>(rows) * pair_bytes > g->rows_pin_bytes) {
+    if ((rc = tfb::cu(cudaStreamSynchronize(g->stream)))) return rc;
+    if (g->rows_pin) cudaFreeHost(g->rows_pin);
+    g->rows_pin = nullptr;
+    g->rows_pin_bytes = 0;
+    const size_t want = static_cast<size_t>(rows) * pair_bytes;
+    if ((rc = tfb::cu(cudaHostAlloc(&g->rows_pin, want, cudaHostAllocMapped)))) return rc;
+    g->rows_pin_bytes = want;
+  }
+  const tfb::Mem kx = cols > 0 ? tfb::classify(hx, g->device) : tfb::Mem::kPageable;
+  const tfb::Mem ky = dot && cols > 0 ? tfb::classify(hy, g->device) : kx;
+  if (kx == tfb::Mem::kOtherDevice || ky == tfb::Mem::kOtherDevice) return TF_EINVAL_ARG;
+  if (kx != tfb::Mem::kPageable || ky != tfb::Mem::kPageable) {
+    if ((rc = tfb::cu(cudaEventRecord(g->entry, static_cast<cudaStream_t>(after_stream))))) return rc;
+    if ((rc = tfb::cu(cudaStreamWaitEvent(g->stream, g->entry, 0)))) return rc;
+    if ((rc = tfb::cu(cudaStreamWaitEvent(g->cstream, g->entry, 0)))) return rc;
+  }
+  if (kx == tfb::Mem::kDevice && ky == tfb::Mem::kDevice) {
+    rc = tf_reduce_rows(method, dtype, hx, hy, rows, cols, ldx, ldy, lg, g->rows_pin, g->partials,
+                        g->partials_bytes, g->counters, g->counters_len, g->stream);
+  } else if (kx == tfb::Mem::kDevice || ky == tfb::Mem::kDevice) {
+    return TF_EINVAL_ARG;  // mixed host/device operands
+  } else {
+    // Row blocks, packed (leading dimension = cols) into the staging slots; the
+    // copies of block b+1 (copy stream) overlap the reduction of block b.
+    const size_t row_bytes = static_cast<size_t>(cols) * item;
+    const size_t want = std::min(static_cast<size_t>(rows) * row_bytes, g->chunk_target);
+    if ((rc = tfb::grow_slots(g, std::max(want, row_bytes)))) return rc;
+    const int64_t block = std::max<int64_t>(1, static_cast<int64_t>(g->chunk / std::max<size_t>(row_bytes, 1)));
+    const int64_t nblocks = (rows + block - 1) / block;
+    const auto* cx = static_cast<const char*>(hx);
+    const auto* cy = static_cast<const char*>(hy);
+    auto stage_block = [&](int b, int k, const char* src, int64_t ld, int64_t r0, int64_t nr, tfb::Mem kind,
+                           bool wait) -> int {
+      const char* s0 = src + static_cast<size_t>(r0) * ld * item;
+      if (ld == cols) return tfb::stage(g, g->cstream, b, k, s0, static_cast<size_t>(nr) * row_bytes, kind, wait);
+      char* d = g->dev[b] + k * g->chunk;
+      if (kind == tfb::Mem::kPinned)  // pitched DMA packs the rows
+        return tfb::cu(cudaMemcpy2DAsync(d, row_bytes, s0, ld * item, row_bytes, nr, cudaMemcpyHostToDevice,
+                                         g->cstream));
+      if (wait) {
+        int e = tfb::cu(cudaEventSynchronize(g->h2d_done[b]));
+        if (e) return e;
+      }
+      char* p = g->pin[b] + k * g->chunk;
+      for (int64_t r = 0; r < nr; ++r) g->pool->copy(p + r * row_bytes, s0 + static_cast<size_t>(r) * ld * item, row_bytes);
+      return tfb::cu(cudaMemcpyAsync(d, p, static_cast<size_t>(nr) * row_bytes, cudaMemcpyHostToDevice, g->cstream));
+    };
+    for (int64_t c = 0; c < nblocks && rc == TF_OK; ++c) {
+      const int b = static_cast<int>(c & 1);
+      const int64_t r0 = c * block;
+      const int64_t nr = std::min(rows, r0 + block) - r0;
+      if (c >= 2 && (rc = tfb::cu(cudaStreamWaitEvent(g->cstream, g->k_done[b], 0)))) break;
+      if ((rc = stage_block(b, 0, cx, ldx, r0, nr, kx, c >= 2))) break;
+      if (dot && (rc = stage_block(b, 1, cy, ldy, r0, nr, ky, c >= 2))) break;
+      if ((rc = tfb::cu(cudaEventRecord(g->h2d_done[b], g->cstream)))) break;
+      if ((rc = tfb::cu(cudaStreamWaitEvent(g->stream, g->h2d_done[b], 0)))) break;
+      rc = tf_reduce_rows(method, dtype, g->dev[b], dot ? g->dev[b] + g->chunk : nullptr, nr, cols, cols, cols, lg,
+                          static_cast<char*>(g->rows_pin) + static_cast<size_t>(r0) * pair_bytes, g->partials,
+                          g->partials_bytes, g->counters, g->counters_len, g->stream);
+      if (rc == TF_OK) rc = tfb::cu(cudaEventRecord(g->k_done[b], g->stream));
+    }
+  }
+  if (rc) {
+    cudaStreamSynchronize(g->cstream);
+    cudaStreamSynchronize(g->stream);
+    return rc;
+  }
+  if ((rc = tfb::cu(cudaStreamSynchronize(g->stream)))) return rc;
+  std::memcpy(out_pairs_host, g->rows_pin, static_cast<size_t>(rows) * pair_bytes);
   return TF_OK;
 }
 

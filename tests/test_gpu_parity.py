@@ -698,3 +698,36 @@ def test_wrappers_accept_strided_numpy_lists_and_views(tfb, oracle, cuda):
     r = tfb.sum_wide(f32[1::3])
     w = oracle.emulate(1, np.ascontiguousarray(f32[1::3]))
     assert _hex(r.value) == _hex(w[0]) and type(r.value) is np.float64
+
+
+def test_host_rows_engine_equals_device_rows(tfb, oracle, cuda):
+    """tf_host_reduce_rows (row blocks staged + overlapped, pitched DMA for pinned strided
+    input) == tf_reduce_rows on the device copy, bit for bit; many blocks via 1 MiB slots."""
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    eng = _lib.host_engine(0, chunk_bytes=1 << 20, threads=3)
+    for dt, code in ((np.float32, 0), (np.float64, 1)):
+        for rows, cols, ld in ((37, 70_001, 70_001), (9, 4_999, 5_000), (300, 1_000, 1_003), (2, 3, 3)):
+            base = oracle.lcg_fill("mmix", rows * ld, 121, dt, True).reshape(rows, ld)
+            ybase = oracle.lcg_fill("nr", rows * ld, 122, dt, True).reshape(rows, ld)
+            want = {}
+            for m in (0, 2, 3, 4):
+                meth = list(tfb.Method)[m]
+                xd = torch.from_numpy(base).to(cuda)[:, :cols]
+                yd = torch.from_numpy(ybase).to(cuda)[:, :cols]
+                want[m] = tfb.reduce_rows(meth, xd, yd).cpu().numpy()
+            for pinned in (False, True):
+                xt = torch.from_numpy(base)
+                yt = torch.from_numpy(ybase)
+                if pinned:
+                    xt, yt = xt.pin_memory(), yt.pin_memory()
+                xs, ys = xt[:, :cols], yt[:, :cols]
+                for m in (0, 2, 3, 4):
+                    out = np.empty((rows, 2), dt)
+                    rc = L.tf_host_reduce_rows(eng, m, code, xs.data_ptr(), ys.data_ptr(), rows, cols, ld, ld, 0,
+                                               out.ctypes.data, None)
+                    assert rc == 0, L.tf_strerror(rc)
+                    assert np.array_equal(out.view(np.uint8), want[m].view(np.uint8)), (dt, rows, cols, ld, pinned, m)
+                    # and through the public API (default engine)
+                    got = tfb.reduce_rows(list(tfb.Method)[m], xs, ys).cpu().numpy()
+                    assert np.array_equal(got.view(np.uint8), want[m].view(np.uint8)), (dt, rows, cols, "api")
