@@ -33,6 +33,9 @@ constexpr int kLimbs = 72;   // 72 * 32 = 2304 bit positions >= 2098 + 64 carry 
 #ifndef TFB_EXACT_DUAL
 #define TFB_EXACT_DUAL 0
 #endif
+#ifndef TFB_EXACT_U
+#define TFB_EXACT_U 2  // 16-byte vectors per operand loaded ahead of the cascades
+#endif
 #ifndef TFB_EXACT_MINB
 #define TFB_EXACT_MINB 4
 #endif
@@ -291,7 +294,7 @@ __global__ void __launch_bounds__(kExactThreads, kExactMinBlocks) exact_kernel(
   // run (the flush atomics keep the compiler from prefetching on its own).
   using VT = typename ExVec<T>::type;
   constexpr int VB = ExVec<T>::V;
-  constexpr int U = 2;
+  constexpr int U = TFB_EXACT_U;
   const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
                        (!DOT || (reinterpret_cast<uintptr_t>(y) & 15u) == 0);
   int64_t scalar_from = 0;
