@@ -76,14 +76,18 @@ __device__ __forceinline__ Pair<A> ld_pair_cg(const Pair<A>* p) {
 #ifndef TFB_RETIRE_ACQREL
 #define TFB_RETIRE_ACQREL 0  // both forms compile to MEMBAR.ALL.GPU + ATOM + CCTL.IVALL on sm_100a
 #endif
-__device__ __forceinline__ unsigned retire_ticket(unsigned* counter) {
+// `count` unit pairs of one row are retired at once (the TMA loader: a CTA
+// stores the pairs of all its leaves of the row with plain stores and takes ONE
+// ticket when it leaves the row, no fence round trip per leaf); the CTA whose
+// ticket completes the row's count builds the row tree.
+__device__ __forceinline__ unsigned retire_ticket(unsigned* counter, unsigned count = 1u) {
 #if TFB_RETIRE_ACQREL
   unsigned prev;
-  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(counter) : "memory");
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;" : "=r"(prev) : "l"(counter), "r"(count) : "memory");
   return prev;
 #else
   __threadfence();
-  return atomicAdd(counter, 1u);
+  return atomicAdd(counter, count);
 #endif
 }
 __device__ __forceinline__ void acquire_fence() {
@@ -301,8 +305,11 @@ template <> struct Unroll<double> { static constexpr int value = TFB_UNROLL_F64;
 // not depend on S — S only balances the grid over the SMs.
 // mode 0: write unit pairs to partials[u] only.  mode 1: fused — the CTA that
 // retires a row's last unit builds the row tree into out[r].
+#ifndef TFB_LDG_MINB
+#define TFB_LDG_MINB 1  // min resident CTAs per SM the LDG kernel is compiled for (tuning builds only)
+#endif
 template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1>
-__global__ void __launch_bounds__(NT) leaves_kernel(
+__global__ void __launch_bounds__(NT, NT == kThreads && UF == 1 ? TFB_LDG_MINB : 1) leaves_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy,
     int64_t rows, int64_t cols, int leaf_log2, int64_t P,
     Pair<typename Acc<M, T>::type>* __restrict__ partials, unsigned* __restrict__ counters,

@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) leaves_tma_kernel(
   const int t = threadIdx.x;
   int slot = 0;
   uint32_t phase = 0;
+  unsigned pending = 0;  // leaf pairs of the current row stored but not yet retired
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
     const int64_t r = u / P, l = u - r * P;
     const int64_t start = l * Lelems;
@@ -156,10 +157,12 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) leaves_tma_kernel(
       finish_root<M, A, 1, kTmaConsumers>(st, out + r, peer, epoch, red);
       continue;
     }
-    if (t == 0) {
-      partials[u] = st;
-      s_last = (retire_ticket(&counters[r]) == static_cast<unsigned>(P - 1));
-    }
+    if (t == 0) partials[u] = st;
+    ++pending;
+    const int64_t un = u + gridDim.x;
+    if (un < units && un / P == r) continue;  // one ticket per row per CTA (reduce.cu:retire_ticket)
+    if (t == 0) s_last = (retire_ticket(&counters[r], pending) + pending == static_cast<unsigned>(P));
+    pending = 0;
     group_sync<1, kTmaConsumers>();
     if (s_last) {
       acquire_fence();
