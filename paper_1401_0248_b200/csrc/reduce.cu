@@ -305,11 +305,16 @@ template <> struct Unroll<double> { static constexpr int value = TFB_UNROLL_F64;
 // not depend on S — S only balances the grid over the SMs.
 // mode 0: write unit pairs to partials[u] only.  mode 1: fused — the CTA that
 // retires a row's last unit builds the row tree into out[r].
-#ifndef TFB_LDG_MINB
-#define TFB_LDG_MINB 1  // min resident CTAs per SM the LDG kernel is compiled for (tuning builds only)
+// TFB_LDG_MINB (tuning builds only): min resident CTAs per SM the 256-thread
+// LDG kernel is compiled for.  Unset = plain __launch_bounds__(NT): an explicit
+// minimum of 1 makes ptxas spend up to 104 registers (3 CTAs/SM instead of 5).
+#ifdef TFB_LDG_MINB
+#define TFB_LDG_BOUNDS(NT, UF) __launch_bounds__(NT, (NT) == kThreads && (UF) == 1 ? TFB_LDG_MINB : 1)
+#else
+#define TFB_LDG_BOUNDS(NT, UF) __launch_bounds__(NT)
 #endif
 template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1>
-__global__ void __launch_bounds__(NT, NT == kThreads && UF == 1 ? TFB_LDG_MINB : 1) leaves_kernel(
+__global__ void TFB_LDG_BOUNDS(NT, UF) leaves_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy,
     int64_t rows, int64_t cols, int leaf_log2, int64_t P,
     Pair<typename Acc<M, T>::type>* __restrict__ partials, unsigned* __restrict__ counters,
