@@ -109,6 +109,13 @@ int tf_set_leaf_split(int split);
  * the initial value. */
 int tf_set_tail(int tail);
 
+/* Tuning knob (process-wide): kernel for tf_reduce_rows when every row fits one
+ * leaf (cols <= 2^leaf_log2) — 0 = automatic (rows of <= 16 KiB per operand: a
+ * group of 1..32 lanes per row, rows.cuh; longer rows: one CTA per row), 1 =
+ * always one CTA per row, 2 = always lane groups.  Identical results; env
+ * TFB_ROWS sets the initial value. */
+int tf_set_rows_kernel(int kind);
+
 /* Human-readable description of the calling thread's last grid-reduction
  * launch (kernel, template arguments, grid, block, units, leaf size). */
 const char* tf_last_launch(void);

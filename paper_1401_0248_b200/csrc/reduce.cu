@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(kThreads) noread_kernel(const T* __restrict__ 
 }  // namespace tfb
 #include "tma.cuh"
 #include "small.cuh"
+#include "rows.cuh"
 namespace tfb {
 
 // ---------------------------------------------------------------------------
@@ -705,6 +706,42 @@ static int launch_small(const T* px, const T* py, int64_t n, int64_t P, void* ou
   return check_launch();
 }
 
+// Rows family, one leaf per row: 0 = auto (the short-row kernel for rows of
+// <= kShortRowMaxBytes per operand), 1 = always the CTA-per-leaf kernels,
+// 2 = always the short-row kernel.  Identical results; env TFB_ROWS or
+// tf_set_rows_kernel() choose.
+constexpr int64_t kShortRowMaxBytes = int64_t(16) << 10;
+static int g_rows_kernel = -1;
+static int rows_kernel_choice() {
+  if (g_rows_kernel < 0) {
+    const char* e = getenv("TFB_ROWS");
+    g_rows_kernel = e ? atoi(e) : 0;
+  }
+  return g_rows_kernel;
+}
+
+template <int M, typename T, bool DOT, bool VEC>
+static int launch_rows_short(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
+                             int leaf_log2, void* out, cudaStream_t stream) {
+  using A = typename Acc<M, T>::type;
+  constexpr int V = Vec<T>::V;
+  auto kern = &rows_short_kernel<M, T, DOT, VEC>;
+  const int g_log2 = rows_short_glog2(cols, V);
+  const int64_t K = (cols + int64_t(kThreads) * V - 1) / (int64_t(kThreads) * V);
+  TFB_CHECK(K <= (int64_t(1) << leaf_log2) / (int64_t(kThreads) * V));
+  const int64_t rows_per_cta = int64_t(kWarps) * (32 >> g_log2);
+  const int64_t want = (rows + rows_per_cta - 1) / rows_per_cta;
+  const int64_t slots = static_cast<int64_t>(device_sms()) * occupancy_of(reinterpret_cast<const void*>(kern));
+  const unsigned grid = static_cast<unsigned>(want < slots ? want : slots);
+  snprintf(g_last_launch, sizeof(g_last_launch),
+           "rows_short_kernel<%s,%s,%s,%s> grid=%u block=%d rows=%lld cols=%lld lanes/row=%d leaf_log2=%d",
+           method_tag(M), sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", VEC ? "ldg128" : "scalar", grid,
+           kThreads, static_cast<long long>(rows), static_cast<long long>(cols), 1 << g_log2, leaf_log2);
+  kern<<<grid, kThreads, 0, stream>>>(px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2,
+                                      static_cast<Pair<A>*>(out));
+  return check_launch();
+}
+
 template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1>
 static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                             int leaf_log2, int64_t P, void* partials, void* counters, void* out, int fused,
@@ -748,6 +785,13 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
       (int64_t(1) << leaf_log2) == int64_t(kThreads) * Vec<T>::V)
     return vec ? launch_small<M, T, DOT, true>(px, py, cols, P, out, stream)
                : launch_small<M, T, DOT, false>(px, py, cols, P, out, stream);
+  // Many rows of at most one leaf each: a group of lanes per row (rows.cuh).
+  if (fused && !peer && rows > 1 && P == 1) {
+    const int rk = rows_kernel_choice();
+    if (rk == 2 || (rk == 0 && cols * int64_t(sizeof(T)) <= kShortRowMaxBytes))
+      return vec ? launch_rows_short<M, T, DOT, true>(px, py, ldx, ldy, rows, cols, leaf_log2, out, stream)
+                 : launch_rows_short<M, T, DOT, false>(px, py, ldx, ldy, rows, cols, leaf_log2, out, stream);
+  }
   // partial-pair capacity the kernels may write: callers of the leaves-only mode
   // (tf_reduce_leaves) promise ceil(n/L) pairs
   const int64_t cap = fused ? (partial_capacity < 0 ? 0 : partial_capacity) : units;
@@ -949,6 +993,12 @@ int tf_set_tail(int tail) {
 int tf_set_loader(int loader) {
   if (loader < 0 || loader > 8 || loader == 4 || loader == 5) return TF_EINVAL_ARG;
   g_loader = loader;
+  return TF_OK;
+}
+
+int tf_set_rows_kernel(int kind) {
+  if (kind < 0 || kind > 2) return TF_EINVAL_ARG;
+  g_rows_kernel = kind;
   return TF_OK;
 }
 

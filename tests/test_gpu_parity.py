@@ -187,6 +187,60 @@ def test_rows_equal_per_row_reduce_and_emulator(tfb, oracle, cuda):
                 _same(got[r], tfb.reduce(meth, X[r], Y[r], leaf_log2=lg).cpu().numpy(), ("row vs 1-D", r))
 
 
+SHORT_COLS = [1, 3, 4, 7, 16, 31, 33, 64, 100, 128, 255, 256, 257, 1000, 1024, 1025, 2049, 4095, 4096]
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_rows_short_kernel_matches_emulator(tfb, oracle, cuda, dt):
+    """rows.cuh (lane groups of 1..32 per row, every row inside one leaf) == the oracle's
+    restatement of the 256-chain leaf tree, bit for bit, for every method x sum/dot x
+    TwoProduct; == the CTA-per-leaf kernel incl. signed zeros (all -0 rows, zero rows);
+    aligned, strided-aligned and misaligned (scalar path) leading dimensions.  Leaf 2^13, so
+    every row fits one leaf and the longer rows take several vectors per chain (K = 2..8)."""
+    L = tfb._lib.lib()
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    try:
+        for cols in SHORT_COLS:
+            rows = 67
+            Xh = oracle.lcg_fill("mmix", rows * cols, 40 + cols % 11, dt, True).reshape(rows, cols)
+            Yh = oracle.lcg_fill("nr", rows * cols, 50 + cols % 7, dt, True).reshape(rows, cols)
+            Xh[5] = -0.0  # a row summing to -0 in every order
+            Xh[6] = 0.0
+            Xh[7, 1::2] = -Xh[7, 0::2][: Xh[7, 1::2].shape[0]]  # cancelling neighbours
+            X, Y = torch.from_numpy(Xh).to(cuda), torch.from_numpy(Yh).to(cuda)
+            cases = [(m, list(tfb.Method)[m], False) for m in _methods(dt)]
+            cases += [(5, tfb.Method.TWOFOLD_FAST, True), (6, tfb.Method.TWOFOLD_RIGOROUS, True)]
+            for m, meth, tp in cases:
+                for yy, yyh in ((None, None), (Y, Yh)):
+                    if tp and yy is None:
+                        continue
+                    ev, ee = oracle.emulate_rows(m, Xh, yyh, leaf_log2=13)
+                    L.tf_set_rows_kernel(2)
+                    got = tfb.reduce_rows(meth, X, yy, leaf_log2=13, track_product=tp).cpu().numpy()
+                    desc = L.tf_last_launch().decode()
+                    assert "rows_short_kernel" in desc, (dt, cols, m, desc)
+                    L.tf_set_rows_kernel(1)
+                    cta = tfb.reduce_rows(meth, X, yy, leaf_log2=13, track_product=tp).cpu().numpy()
+                    assert np.array_equal(got.view(np.uint8), cta.view(np.uint8)), (dt, cols, m, yy is None)
+                    for r in range(rows):
+                        _same(got[r], (ev[r], ee[r]), (dt, cols, m, r, yy is None))
+        # leading dimensions: aligned ld > cols (vector path) and a 1-element offset (scalar path)
+        base = torch.from_numpy(oracle.lcg_fill("mmix", 41 * 1040, 61, dt, True).reshape(41, 1040)).to(cuda)
+        for view in (base[:, :1000], base[:, 1:1001], base[:, 3:20]):
+            vh = np.ascontiguousarray(view.cpu().numpy())
+            for m in (2, 3, 4):
+                L.tf_set_rows_kernel(2)
+                got = tfb.reduce_rows(list(tfb.Method)[m], view).cpu().numpy()
+                ev, ee = oracle.emulate_rows(m, vh)
+                for r in range(41):
+                    _same(got[r], (ev[r], ee[r]), (dt, view.shape, view.storage_offset(), m, r))
+    finally:
+        L.tf_set_rows_kernel(0)
+    # the auto choice takes the lane-group kernel for short rows
+    tfb.reduce_rows(tfb.Method.TWOFOLD_FAST, torch.ones(1000, 64, dtype=tdt, device=cuda))
+    assert "rows_short_kernel" in L.tf_last_launch().decode()
+
+
 def test_rows_strided_leading_dimension(tfb, oracle, cuda):
     base = tfb.rows_scaled_normal(9, 5000, seed=4, stream=0, dtype=torch.float32)
     X = base[:, :4999]  # ld = 5000 > cols: 4-byte misaligned rows -> scalar path
