@@ -706,11 +706,16 @@ static int launch_small(const T* px, const T* py, int64_t n, int64_t P, void* ou
   return check_launch();
 }
 
-// Rows family, one leaf per row: 0 = auto (the short-row kernel for rows of
-// <= kShortRowMaxBytes per operand), 1 = always the CTA-per-leaf kernels,
-// 2 = always the short-row kernel.  Identical results; env TFB_ROWS or
-// tf_set_rows_kernel() choose.
+// Rows family, one leaf per row: 0 = auto, 1 = always the CTA-per-leaf
+// kernels, 2 = always the short-row kernel.  Identical results; env TFB_ROWS or
+// tf_set_rows_kernel() choose.  Auto (measured, scripts/rows_shapes.py): lane
+// groups for 16-byte aligned rows of <= 16 KiB per operand (5.6-6.3 TB/s from
+// 16 to 4096 f32 columns, where a CTA per row reaches 0.07-5.8) and for
+// misaligned rows of < 256 elements; a CTA per row above (LDG 6.3-6.5 TB/s
+// from 16 to 128 KiB rows; the TMA pipeline from 256 KiB rows, cfg4).
 constexpr int64_t kShortRowMaxBytes = int64_t(16) << 10;
+constexpr int64_t kShortRowMaxScalarCols = 256;
+constexpr int64_t kTmaRowMinBytes = int64_t(256) << 10;
 static int g_rows_kernel = -1;
 static int rows_kernel_choice() {
   if (g_rows_kernel < 0) {
@@ -720,7 +725,7 @@ static int rows_kernel_choice() {
   return g_rows_kernel;
 }
 
-template <int M, typename T, bool DOT, bool VEC>
+template <int M, typename T, bool DOT, int VEC>
 static int launch_rows_short(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                              int leaf_log2, void* out, cudaStream_t stream) {
   using A = typename Acc<M, T>::type;
@@ -735,8 +740,9 @@ static int launch_rows_short(const T* px, const T* py, int64_t ldx, int64_t ldy,
   const unsigned grid = static_cast<unsigned>(want < slots ? want : slots);
   snprintf(g_last_launch, sizeof(g_last_launch),
            "rows_short_kernel<%s,%s,%s,%s> grid=%u block=%d rows=%lld cols=%lld lanes/row=%d leaf_log2=%d",
-           method_tag(M), sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", VEC ? "ldg128" : "scalar", grid,
-           kThreads, static_cast<long long>(rows), static_cast<long long>(cols), 1 << g_log2, leaf_log2);
+           method_tag(M), sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum",
+           VEC == 2 ? "ldg256" : VEC == 1 ? "ldg128" : "scalar", grid, kThreads, static_cast<long long>(rows),
+           static_cast<long long>(cols), 1 << g_log2, leaf_log2);
   kern<<<grid, kThreads, 0, stream>>>(px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2,
                                       static_cast<Pair<A>*>(out));
   return check_launch();
@@ -788,9 +794,16 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
   // Many rows of at most one leaf each: a group of lanes per row (rows.cuh).
   if (fused && !peer && rows > 1 && P == 1) {
     const int rk = rows_kernel_choice();
-    if (rk == 2 || (rk == 0 && cols * int64_t(sizeof(T)) <= kShortRowMaxBytes))
-      return vec ? launch_rows_short<M, T, DOT, true>(px, py, ldx, ldy, rows, cols, leaf_log2, out, stream)
-                 : launch_rows_short<M, T, DOT, false>(px, py, ldx, ldy, rows, cols, leaf_log2, out, stream);
+    if (rk == 2 || (rk == 0 && (vec ? cols * int64_t(sizeof(T)) <= kShortRowMaxBytes
+                                     : cols < kShortRowMaxScalarCols))) {
+      auto a32 = [](const void* p, int64_t ld) {
+        return (reinterpret_cast<uintptr_t>(p) & 31u) == 0 && (ld * int64_t(sizeof(T))) % 32 == 0;
+      };
+      if (vec && a32(x, ldx) && (!DOT || a32(y, ldy)))
+        return launch_rows_short<M, T, DOT, 2>(px, py, ldx, ldy, rows, cols, leaf_log2, out, stream);
+      return vec ? launch_rows_short<M, T, DOT, 1>(px, py, ldx, ldy, rows, cols, leaf_log2, out, stream)
+                 : launch_rows_short<M, T, DOT, 0>(px, py, ldx, ldy, rows, cols, leaf_log2, out, stream);
+    }
   }
   // partial-pair capacity the kernels may write: callers of the leaves-only mode
   // (tf_reduce_leaves) promise ceil(n/L) pairs
@@ -810,9 +823,13 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
   int loader = loader_choice();
   if (loader == 0) {
     const int64_t bytes = rows * cols * static_cast<int64_t>(sizeof(T)) * (DOT ? 2 : 1);
-    // the table is measured on 1-D arrays; the row family (one unit per short row)
-    // streams best with the TMA pipeline once it is large (cfg4: 295 vs 303 us)
-    loader = (rows > 1 && DOT && bytes >= (int64_t(512) << 20)) ? 2 : auto_loader(M, sizeof(T) == 8, DOT, bytes);
+    // the table is measured on 1-D arrays.  Rows: below kTmaRowMinBytes per row the
+    // TMA rings never fill (1.8-2.0 TB/s at 16-64 KiB rows): LDG; long rows stream
+    // like 1-D arrays, and large row-wise dots take the TMA pipeline (cfg4: 295 vs 303 us)
+    const bool long_rows = cols * int64_t(sizeof(T)) >= kTmaRowMinBytes;
+    if (rows > 1 && !long_rows) loader = 1;
+    else if (rows > 1 && DOT && bytes >= (int64_t(512) << 20)) loader = 2;
+    else loader = auto_loader(M, sizeof(T) == 8, DOT, bytes);
   }
   if (vec && fused && S == 1) {
     switch (loader) {

@@ -18,8 +18,47 @@
 
 namespace tfb {
 
-template <int M, typename T, bool DOT, bool VEC>
-__global__ void __launch_bounds__(kThreads) rows_short_kernel(
+#ifndef TFB_RS_MINB
+#define TFB_RS_MINB 0  // tuning builds: min resident CTAs per SM (0 = unconstrained, measured best)
+#endif
+#ifndef TFB_RS_PARTS
+#define TFB_RS_PARTS 0  // batches the lane's 8 vectors per k are loaded in (0 = f32: 2, f64: 1; measured)
+#endif
+#if TFB_RS_MINB > 0
+#define TFB_RS_BOUNDS __launch_bounds__(kThreads, TFB_RS_MINB)
+#else
+#define TFB_RS_BOUNDS __launch_bounds__(kThreads)
+#endif
+
+// 32-byte streaming loads (LDG.E...256): lane blocks are 128 bytes apart, so a
+// 16-byte load would use half of every 32-byte sector it touches (and, with no
+// L1 allocation, fetch each sector twice); 32 bytes per lane use all of it.
+__device__ __forceinline__ void ld_stream32(const float4* p, float4& a, float4& b) {
+  asm("ld.global.nc.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+}
+__device__ __forceinline__ void ld_stream32(const double2* p, double2& a, double2& b) {
+  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+      : "l"(p));
+}
+
+// One 16-byte vector through a chain (elements in order).
+template <int M, typename T, bool DOT>
+__device__ __forceinline__ void chain_vec(Pair<typename Acc<M, T>::type>& st, const typename Vec<T>::type& a,
+                                          const typename Vec<T>::type& b) {
+#pragma unroll
+  for (int q = 0; q < Vec<T>::V; ++q) {
+    if constexpr (DOT) accumulate<M, T, true>(st, vget(a, q), vget(b, q));
+    else accumulate<M, T, false>(st, vget(a, q), T(0));
+  }
+}
+
+// VEC: 0 = element loads (misaligned rows), 1 = 16-byte loads (16-byte aligned
+// rows), 2 = 32-byte loads (32-byte aligned rows).  Same elements, same order.
+template <int M, typename T, bool DOT, int VEC>
+__global__ void TFB_RS_BOUNDS rows_short_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
     int K, int g_log2, Pair<typename Acc<M, T>::type>* __restrict__ out) {
   using A = typename Acc<M, T>::type;
@@ -44,25 +83,62 @@ __global__ void __launch_bounds__(kThreads) rows_short_kernel(
       for (int k = 0; k < K; ++k) {
         const int64_t e0 = (int64_t(k) * kThreads + kChains * j) * V;  // this lane's block of 8 vectors
         if (e0 >= cols) break;
-        if (VEC && e0 + kChains * V <= cols) {
-          TFB_CHECK((reinterpret_cast<uintptr_t>(xr + e0) & 15u) == 0);
+        const int64_t rem = cols - e0;  // > 0
+        if (VEC != 0 && rem >= kChains * V) {
+          TFB_CHECK((reinterpret_cast<uintptr_t>(xr + e0) & (VEC == 2 ? 31u : 15u)) == 0);
+          const VT* xv = reinterpret_cast<const VT*>(xr + e0);
+          const VT* yv = DOT ? reinterpret_cast<const VT*>(yr + e0) : nullptr;
+          constexpr int kParts = TFB_RS_PARTS > 0 ? TFB_RS_PARTS : (sizeof(T) == 8 ? 1 : 2);
+          constexpr int kPer = kChains / kParts;
+#pragma unroll
+          for (int h = 0; h < kParts; ++h) {  // batches of vectors: loads first, then the chains
+            VT a[kPer], b[kPer];
+            if constexpr (VEC == 2) {
+#pragma unroll
+              for (int c = 0; c < kPer; c += 2) {
+                ld_stream32(xv + kPer * h + c, a[c], a[c + 1]);
+                if constexpr (DOT) ld_stream32(yv + kPer * h + c, b[c], b[c + 1]);
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < kPer; ++c) {
+                a[c] = ld_stream(xv + kPer * h + c);
+                if constexpr (DOT) b[c] = ld_stream(yv + kPer * h + c);
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < kPer; ++c) chain_vec<M, T, DOT>(ch[kPer * h + c], a[c], b[c]);
+          }
+        } else if (VEC != 0) {
+          // partial block (the row's end): whole vectors where they fit, then the
+          // elements of the last partial vector — each chain still in element order
           const VT* xv = reinterpret_cast<const VT*>(xr + e0);
           const VT* yv = DOT ? reinterpret_cast<const VT*>(yr + e0) : nullptr;
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {  // two halves of 4 vectors: loads first, then the chains
-            VT a[4], b[4];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              a[c] = ld_stream(xv + 4 * h + c);
-              if constexpr (DOT) b[c] = ld_stream(yv + 4 * h + c);
+          for (int c = 0; c < kChains; c += 2) {
+            const int64_t o = int64_t(c) * V;
+            if (o >= rem) break;
+            VT a0, a1, b0, b1;
+            if (VEC == 2 && o + 2 * V <= rem) {
+              ld_stream32(xv + c, a0, a1);
+              if constexpr (DOT) ld_stream32(yv + c, b0, b1);
+              chain_vec<M, T, DOT>(ch[c], a0, b0);
+              chain_vec<M, T, DOT>(ch[c + 1], a1, b1);
+              continue;
             }
 #pragma unroll
-            for (int c = 0; c < 4; ++c)
+            for (int cc = c; cc < c + 2; ++cc) {
+              const int64_t oo = int64_t(cc) * V;
+              if (oo + V <= rem) {
+                a0 = ld_stream(xv + cc);
+                if constexpr (DOT) b0 = ld_stream(yv + cc);
+                chain_vec<M, T, DOT>(ch[cc], a0, b0);
+              } else {
 #pragma unroll
-              for (int q = 0; q < V; ++q) {
-                if constexpr (DOT) accumulate<M, T, true>(ch[4 * h + c], vget(a[c], q), vget(b[c], q));
-                else accumulate<M, T, false>(ch[4 * h + c], vget(a[c], q), T(0));
+                for (int q = 0; q < V; ++q)
+                  if (oo + q < rem) accumulate<M, T, DOT>(ch[cc], xr[e0 + oo + q], DOT ? yr[e0 + oo + q] : T(0));
               }
+            }
           }
         } else {
 #pragma unroll
