@@ -53,6 +53,45 @@ def test_fuzz_grid_vs_emulator(tfb, oracle, cuda):
         L.tf_set_leaf_split(0)
 
 
+def test_fuzz_rows_vs_emulator(tfb, oracle, cuda):
+    """Random row-wise reductions (rows x cols, leading dimension / offset, leaf size,
+    method, sum/dot, TwoProduct, rows kernel auto / CTA per row / lane groups) == the
+    oracle's per-row restatement of the tree, bit for bit."""
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    rng = np.random.default_rng(20261021)
+    try:
+        for case in range(120):
+            dt = np.float32 if rng.random() < 0.5 else np.float64
+            methods = (0, 1, 2, 3, 4) if dt == np.float32 else (0, 2, 3, 4)
+            m = int(rng.choice(methods))
+            dot = bool(rng.random() < 0.6)
+            tp = dot and m in (2, 3) and rng.random() < 0.3
+            rows = int(rng.integers(2, 400))
+            cols = int(rng.choice([rng.integers(1, 40), rng.integers(40, 1100), rng.integers(1100, 9000)]))
+            pad = int(rng.choice([0, 0, rng.integers(1, 9)]))
+            off = int(rng.integers(0, 2))
+            lo = 10 if dt == np.float32 else 9
+            lg = int(rng.choice([0, 0, rng.integers(lo, 15)]))
+            ld = cols + pad
+            bx = (rng.standard_normal(rows * ld + off) * 2.0 ** rng.integers(-10, 10, rows * ld + off)).astype(dt)
+            by = rng.uniform(-1, 1, rows * ld + off).astype(dt)
+            X = torch.from_numpy(bx).to(cuda)[off:].as_strided((rows, cols), (ld, 1))
+            Y = torch.from_numpy(by).to(cuda)[off:].as_strided((rows, cols), (ld, 1))
+            Xh = np.ascontiguousarray(X.cpu().numpy())
+            Yh = np.ascontiguousarray(Y.cpu().numpy())
+            kind = int(rng.choice([0, 1, 2]))
+            L.tf_set_rows_kernel(kind)
+            meth = list(tfb.Method)[m]
+            got = tfb.reduce_rows(meth, X, Y if dot else None, leaf_log2=lg, track_product=tp).cpu().numpy()
+            ev, ee = oracle.emulate_rows(m + (3 if tp else 0), Xh, Yh if dot else None, lg)
+            for r in range(rows):
+                assert float(got[r, 0]).hex() == float(ev[r]).hex() and float(got[r, 1]).hex() == float(ee[r]).hex(), \
+                    (case, dt, m, dot, tp, rows, cols, ld, off, lg, kind, r, L.tf_last_launch().decode())
+    finally:
+        L.tf_set_rows_kernel(0)
+
+
 def test_small_instance_criterion_c6_on_the_grid(tfb, oracle):
     """|v + e - S| <= 2 eps |S| for the rigorous grid flavor on the reference's C6 instances."""
     def check(data, eps):
