@@ -133,7 +133,9 @@ int tf_set_loader(int loader);
  *   partials: rows * leaves(cols) (value, error) pairs, any contents on entry;
  *   counters: `rows` uint32 retire-tickets, ZERO on entry and left zero on exit
  *             (so a caller can keep one zeroed counter buffer per stream).
- * Only needed when a row spans more than one leaf (*leaves > 1). */
+ * Only needed when a row spans more than one leaf (*leaves > 1): for rows > 1
+ * and *leaves <= 1 both sizes are returned as 0 (a 1-D call with one leaf still
+ * reports its pair slots, which the fused NVLink combine uses). */
 int tf_workspace_size(int method, int dtype, int64_t rows, int64_t cols, int leaf_log2,
                       size_t* partials_bytes, int64_t* counters, int64_t* leaves);
 

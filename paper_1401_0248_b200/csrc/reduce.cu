@@ -1038,9 +1038,12 @@ int tf_workspace_size(int method, int dtype, int64_t rows, int64_t cols, int lea
   int lg;
   if ((rc = resolve_leaf(dtype, rows * cols, leaf_log2, &lg))) return rc;
   const int64_t P = (cols + (int64_t(1) << lg) - 1) >> lg;
-  // sized for the largest leaf split (kMaxSplit unit pairs per leaf)
-  if (partials_bytes) *partials_bytes = static_cast<size_t>(rows * P * kMaxSplit) * pair_bytes(method, dtype);
-  if (counters) *counters = rows;
+  // sized for the largest leaf split (kMaxSplit unit pairs per leaf).  Many rows of one
+  // leaf each need no scratch at all (every row pair is stored straight into out).
+  const bool none = rows > 1 && P <= 1;
+  if (partials_bytes)
+    *partials_bytes = none ? 0 : static_cast<size_t>(rows * P * kMaxSplit) * pair_bytes(method, dtype);
+  if (counters) *counters = none ? 0 : rows;
   if (leaves) *leaves = P;
   return TF_OK;
 }

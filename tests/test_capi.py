@@ -67,7 +67,11 @@ def test_workspace_size(lib):
     # partials are sized for the largest leaf split (4 unit pairs per leaf)
     assert leaves == (1 << 29) >> 16 and pb == 4 * leaves * 16 and cnt == 1
     pb, cnt, leaves = workspace_size(Method.WIDE, torch.float32, 4096, 65536)
-    assert leaves == 1 and pb == 4 * 4096 * 16 and cnt == 4096  # wide pairs are binary64
+    assert leaves == 1 and pb == 0 and cnt == 0  # one leaf per row: pairs go straight to out
+    pb, cnt, leaves = workspace_size(Method.WIDE, torch.float32, 4096, 65537)
+    assert leaves == 2 and pb == 4 * 4096 * 2 * 16 and cnt == 4096  # wide pairs are binary64
+    pb, cnt, leaves = workspace_size(Method.TWOFOLD_FAST, torch.float32, 1, 100)
+    assert leaves == 1 and pb == 4 * 8 and cnt == 1  # 1-D: the pair slots stay (peer combine)
     pb, cnt, leaves = workspace_size(Method.KAHAN, torch.float32, 1, 1 << 24)
     assert leaves == (1 << 24) >> 15 and pb == 4 * leaves * 8
 
