@@ -476,6 +476,7 @@ __global__ void __launch_bounds__(kThreads) noread_kernel(const T* __restrict__ 
 #include "tma.cuh"
 #include "small.cuh"
 #include "rows.cuh"
+#include "seqpipe.cuh"
 namespace tfb {
 
 // ---------------------------------------------------------------------------
@@ -887,9 +888,42 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
 #undef TFB_NT
 }
 
+// Sequential flavors: inputs of at least a few chunks whose operands share
+// their offset modulo 16 bytes stream through the bulk-copy ring (seqpipe.cuh);
+// the rest use the plain one-thread / k-thread kernels.  Same element order.
+template <int M, typename T, bool DOT>
+static int launch_seq_pipe(const void* x, const void* y, int64_t n, int k, void* out, cudaStream_t s) {
+  using A = typename Acc<M, T>::type;
+  constexpr int64_t CE = kSeqChunkBytes / sizeof(T);
+  const uintptr_t mx = reinterpret_cast<uintptr_t>(x) & 15u;
+  if (n < 4 * CE || (DOT && (reinterpret_cast<uintptr_t>(y) & 15u) != mx)) return -1;
+  const int64_t head = static_cast<int64_t>((16u - mx) & 15u) / static_cast<int64_t>(sizeof(T));
+  const int64_t nchunks = (n - head) / CE;
+  auto kern = &seq_pipe_kernel<M, T, DOT>;
+  const size_t smem = SeqSmem<T, DOT>::kBytes;
+  static std::mutex mu;
+  static std::unordered_map<int, bool> ok;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (!ok.count(dev)) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+          cudaSuccess)
+        return record_cuda_error();
+      ok[dev] = true;
+    }
+  }
+  kern<<<1, kSeqThreads, smem, s>>>(static_cast<const T*>(x), static_cast<const T*>(y), n, k, head, nchunks,
+                                     static_cast<Pair<A>*>(out));
+  return check_launch();
+}
+
 template <int M, typename T, bool DOT>
 static int launch_seq(const void* x, const void* y, int64_t n, void* out, cudaStream_t s) {
   using A = typename Acc<M, T>::type;
+  const int rc = launch_seq_pipe<M, T, DOT>(x, y, n, 1, out, s);
+  if (rc >= 0) return rc;
   seq_kernel<M, T, DOT><<<1, 1, 0, s>>>(static_cast<const T*>(x), static_cast<const T*>(y), n,
                                         static_cast<Pair<A>*>(out));
   return check_launch();
@@ -898,6 +932,8 @@ static int launch_seq(const void* x, const void* y, int64_t n, void* out, cudaSt
 template <int M, typename T, bool DOT>
 static int launch_lanes(const void* x, const void* y, int64_t n, int k, void* out, cudaStream_t s) {
   using A = typename Acc<M, T>::type;
+  const int rc = launch_seq_pipe<M, T, DOT>(x, y, n, k, out, s);
+  if (rc >= 0) return rc;
   lanes_kernel<M, T, DOT><<<1, k, 0, s>>>(static_cast<const T*>(x), static_cast<const T*>(y), n, k,
                                           static_cast<Pair<A>*>(out));
   return check_launch();

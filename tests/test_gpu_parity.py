@@ -241,6 +241,31 @@ def test_rows_short_kernel_matches_emulator(tfb, oracle, cuda, dt):
     assert "rows_short_kernel" in L.tf_last_launch().decode()
 
 
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_sequential_flavors_streamed_match_reference_order(tfb, oracle, cuda, dt):
+    """seq and unroll:k on inputs large enough for the bulk-copy ring (seqpipe.cuh):
+    bit-identical to the oracle's restatement of the reference kernels, for every
+    method x sum/dot x TwoProduct, head misalignment 0..3 elements (operands with equal
+    and with different offsets mod 16 bytes, the latter on the plain kernels)."""
+    for n, offx, offy in ((40_000, 0, 0), (100_003, 1, 1), (70_001, 3, 3), (50_000, 1, 2), (1 << 18, 2, 2)):
+        xh = oracle.lcg_fill("mmix", n + 4, 71 + offx, dt, True)
+        yh = oracle.lcg_fill("nr", n + 4, 72 + offy, dt, True)
+        xd, yd = torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda)
+        x, y = xd[offx:offx + n], yd[offy:offy + n]
+        xs, ys = xh[offx:offx + n], yh[offy:offy + n]
+        cases = [(m, list(tfb.Method)[m], False) for m in _methods(dt)]
+        cases += [(5, tfb.Method.TWOFOLD_FAST, True), (6, tfb.Method.TWOFOLD_RIGOROUS, True)]
+        for m, meth, tp in cases:
+            for yy, yyh in ((None, None), (y, ys)):
+                if tp and yy is None:
+                    continue
+                got = tfb.reduce(meth, x, yy, flavor=tfb.Flavor.sequential(), track_product=tp).cpu().numpy()
+                _same(got, oracle.seq(m, xs, yyh), (dt, n, offx, offy, m, "seq"))
+                for k in (2, 4, 16):
+                    got = tfb.reduce(meth, x, yy, flavor=tfb.Flavor.unrolled(k), track_product=tp).cpu().numpy()
+                    _same(got, oracle.lanes(m, xs, yyh, k), (dt, n, offx, offy, m, "lanes", k))
+
+
 def test_rows_strided_leading_dimension(tfb, oracle, cuda):
     base = tfb.rows_scaled_normal(9, 5000, seed=4, stream=0, dtype=torch.float32)
     X = base[:, :4999]  # ld = 5000 > cols: 4-byte misaligned rows -> scalar path
