@@ -13,6 +13,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #define CK(x)                                                                      \
@@ -46,6 +47,35 @@ __global__ void __launch_bounds__(256) gs_kernel(const uint4* __restrict__ p, in
   for (; i < nvec; i += stride) {
     uint4 v = ldv(p + i);
     acc ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (acc == 0x9E3779B9u) sink[0] = acc;
+}
+
+// Grid-stride with 32-byte loads per thread (LDG...256): U loads of 32 B in flight.
+struct u8v { uint4 a, b; };
+__device__ __forceinline__ u8v ldv32(const uint4* p) {
+  u8v v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v.a.x), "=r"(v.a.y), "=r"(v.a.z), "=r"(v.a.w), "=r"(v.b.x), "=r"(v.b.y), "=r"(v.b.z),
+                 "=r"(v.b.w)
+               : "l"(p));
+  return v;
+}
+template <int U>
+__global__ void __launch_bounds__(256) gs32_kernel(const uint4* __restrict__ p, int64_t npairs, unsigned* sink) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  unsigned acc = 0;
+  int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  for (; i + (U - 1) * stride < npairs; i += U * stride) {
+    u8v v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = ldv32(p + 2 * (i + u * stride));
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc ^= v[u].a.x ^ v[u].a.w ^ v[u].b.y ^ v[u].b.z;
+  }
+  for (; i < npairs; i += stride) {
+    const u8v v = ldv32(p + 2 * i);
+    acc ^= v.a.x ^ v.a.w ^ v.b.y ^ v.b.z;
   }
   if (acc == 0x9E3779B9u) sink[0] = acc;
 }
@@ -98,6 +128,32 @@ __global__ void __launch_bounds__(256) leaf_kernel(const uint4* __restrict__ x, 
   if (acc == 0x9E3779B9u) sink[0] = acc;
 }
 
+// Two leaves per 256-thread CTA, 32-byte loads: thread tt (0..127) of half h
+// reads vectors 2tt, 2tt+1 of every 256-vector row of leaf (2*l2 + h).
+template <int U>
+__global__ void __launch_bounds__(256) leaf32_kernel(const uint4* __restrict__ x, const uint4* __restrict__ y,
+                                                     int R, int64_t P, unsigned* sink) {
+  unsigned acc = 0;
+  const int h = threadIdx.x >> 7, tt = threadIdx.x & 127;
+  for (int64_t l2 = blockIdx.x; 2 * l2 < P; l2 += gridDim.x) {
+    const int64_t l = 2 * l2 + h;
+    if (l >= P) break;
+    const uint4* xv = x + l * int64_t(R) * 256 + 2 * tt;
+    const uint4* yv = y + l * int64_t(R) * 256 + 2 * tt;
+    for (int k = 0; k < R; k += U) {
+      u8v a[U], b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a[u] = ldv32(xv + (k + u) * 256);
+        b[u] = ldv32(yv + (k + u) * 256);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) acc ^= a[u].a.x ^ a[u].b.w ^ b[u].a.y ^ b[u].b.z;
+    }
+  }
+  if (acc == 0x9E3779B9u) sink[0] = acc;
+}
+
 struct Pool {
   char* base;
   size_t bytes;
@@ -143,7 +199,8 @@ int main() {
   CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
 
   // total bytes per launch (both operands)
-  const size_t sizes[] = {size_t(8) << 20, size_t(32) << 20, size_t(128) << 20, size_t(512) << 20};
+  const size_t sizes[] = {size_t(8) << 20, size_t(32) << 20, size_t(128) << 20, size_t(512) << 20,
+                          size_t(2048) << 20};
   for (size_t total : sizes) {
     const int slots = static_cast<int>(pool_bytes / total);
     const int reps = slots < 8 ? 8 : (slots > 40 ? 40 : slots);
@@ -157,6 +214,37 @@ int main() {
       printf("grid-stride grid=%u U4 %.2f us %.0f GB/s | U8 %.2f us %.0f GB/s\n", grid, us4, total / us4 / 1e3, us8,
              total / us8 / 1e3);
     }
+    for (int mult : {4, 8}) {
+      const unsigned grid = sms * mult;
+      float a2 = graph_us([&](int i) { gs32_kernel<2><<<grid, 256, 0, s>>>(buf(i), nvec / 2, sink); }, reps, s);
+      float a4 = graph_us([&](int i) { gs32_kernel<4><<<grid, 256, 0, s>>>(buf(i), nvec / 2, sink); }, reps, s);
+      printf("grid-stride 32B grid=%u U2 %.2f us %.0f GB/s | U4 %.2f us %.0f GB/s\n", grid, a2, total / a2 / 1e3, a4,
+             total / a4 / 1e3);
+    }
+    if (getenv("PROBE_GS_ONLY")) continue;
+    for (int leaf_kb : {16, 32, 64, 128}) {
+      const int64_t leaf_bytes = int64_t(leaf_kb) << 10;
+      const int64_t P = (total / 2) / leaf_bytes;
+      const int R = static_cast<int>(leaf_bytes / (16 * 256));
+      if (P < 64) continue;
+      for (int U : {2, 4}) {
+        if (U > R) continue;
+        for (int64_t occ : {int64_t(4), int64_t(8)}) {
+          const int64_t cap = int64_t(sms) * occ;
+          const unsigned grid = static_cast<unsigned>((P + 1) / 2 < cap ? (P + 1) / 2 : cap);
+          auto L = [&](int i) {
+            const uint4* x = buf(i);
+            const uint4* y = x + nvec / 2;
+            if (U == 2) leaf32_kernel<2><<<grid, 256, 0, s>>>(x, y, R, P, sink);
+            else leaf32_kernel<4><<<grid, 256, 0, s>>>(x, y, R, P, sink);
+          };
+          float us = graph_us(L, reps, s);
+          printf("leaf32 %3d KB/operand P=%5lld grid=%u U=%d: %.2f us %.0f GB/s\n", leaf_kb,
+                 static_cast<long long>(P), grid, U, us, total / us / 1e3);
+        }
+      }
+    }
+    if (getenv("PROBE_LEAF32_ONLY")) continue;
     // leaves: operand bytes = total/2; leaf bytes per operand = 2^leaf_log2 * 4 (f32 view)
     for (int leaf_kb : {8, 16, 32, 64, 128, 256}) {
       const int64_t leaf_bytes = int64_t(leaf_kb) << 10;
