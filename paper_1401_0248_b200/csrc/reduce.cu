@@ -217,9 +217,36 @@ __device__ __forceinline__ void consume_batch(Pair<typename Acc<M, T>::type>& st
   }
 }
 
+// Misaligned binary32 operands (both MS elements past a 16-byte boundary): chain t's
+// vector starts MS elements into aligned vector t and ends in aligned vector
+// t + 1 — loaded by the next lane (warp shuffle) or, for lane 31, by itself.
+// Every aligned vector read lies in a 16-byte block holding an element of the
+// leaf, i.e. inside the caller's allocation.
+template <typename T> __device__ __forceinline__ T shfl_down1(T v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+// Element j of chain t's vector: components MS.. of its own aligned vector, then
+// components 0..MS-1 of the next one (nx).
+template <int MS, typename T>
+__device__ __forceinline__ T shifted_get(const typename Vec<T>::type& own, const T (&nx)[MS], int j) {
+  constexpr int V = Vec<T>::V;
+  return MS + j < V ? vget(own, MS + j) : nx[MS + j - V];
+}
+// nx = components 0..MS-1 of the next aligned vector: lane + 1's, or (lane 31)
+// the elements it loaded itself together with its own batch (`edge_vals`).
+template <int MS, typename T>
+__device__ __forceinline__ void next_comps(const typename Vec<T>::type& own, const T (&edge_vals)[MS], bool edge,
+                                           T (&nx)[MS]) {
+#pragma unroll
+  for (int q = 0; q < MS; ++q) {
+    const T v = shfl_down1(vget(own, q));
+    nx[q] = edge ? edge_vals[q] : v;
+  }
+}
+
 // One thread's sequential recurrence over its elements of the leaf at
 // `start` of a row of n elements.  VEC: 16-byte aligned row, full leaf.
-template <int M, typename T, bool DOT, bool VEC, int U>
+// MS > 0 (with VEC false): both operands MS elements past a 16-byte boundary,
+// full leaf: aligned vector loads + one lane shuffle (same elements, same order).
+template <int M, typename T, bool DOT, bool VEC, int U, int MS = 0>
 __device__ __forceinline__ Pair<typename Acc<M, T>::type> leaf_chain(
     const T* __restrict__ x, const T* __restrict__ y, int64_t start, int64_t n, int R, int t) {
   using A = typename Acc<M, T>::type;
@@ -228,6 +255,51 @@ __device__ __forceinline__ Pair<typename Acc<M, T>::type> leaf_chain(
   Pair<A> st = zero_pair<A>();
   const int64_t L = static_cast<int64_t>(R) * kThreads * V;
   TFB_CHECK(t >= 0 && t < kThreads && start >= 0);
+  if constexpr (!VEC && MS > 0) {
+    if (start + L <= n) {
+    TFB_CHECK((reinterpret_cast<uintptr_t>(x + start - MS) & 15u) == 0);
+    const VT* xa = reinterpret_cast<const VT*>(x + start - MS) + t;
+    const VT* ya = DOT ? reinterpret_cast<const VT*>(y + start - MS) + t : nullptr;
+    const bool edge = (threadIdx.x & 31) == 31;
+    constexpr int US = (sizeof(T) == 4 && DOT && MS >= 2 && U > 2) ? U / 2 : U;  // f32 dots: registers
+    int k = 0;
+    for (; k < R; k += US) {
+      const int nu = R - k < US ? R - k : US;
+      VT a[US], b[US];
+      T ea[US][MS], eb[US][MS];
+#pragma unroll
+      for (int u = 0; u < US; ++u) {
+        if (u < nu) {
+          a[u] = ld_stream(xa + static_cast<int64_t>(k + u) * kThreads);
+          if constexpr (DOT) b[u] = ld_stream(ya + static_cast<int64_t>(k + u) * kThreads);
+          if (edge) {  // lane 31: its last MS elements lie in the next warp's first vector
+            const int64_t e = start + (static_cast<int64_t>(k + u) * kThreads + t) * V + (V - MS);
+#pragma unroll
+            for (int q = 0; q < MS; ++q) {
+              ea[u][q] = __ldg(x + e + q);  // measured faster than a no-allocate load here
+              if constexpr (DOT) eb[u][q] = __ldg(y + e + q);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < US; ++u) {
+        if (u < nu) {
+          T an[MS], bn[MS];
+          next_comps<MS, T>(a[u], ea[u], edge, an);
+          if constexpr (DOT) next_comps<MS, T>(b[u], eb[u], edge, bn);
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            if constexpr (DOT)
+              accumulate<M, T, true>(st, shifted_get<MS, T>(a[u], an, j), shifted_get<MS, T>(b[u], bn, j));
+            else accumulate<M, T, false>(st, shifted_get<MS, T>(a[u], an, j), T(0));
+          }
+        }
+      }
+    }
+    return st;
+    }
+  }
   if (VEC && start + L <= n) {
     TFB_CHECK((reinterpret_cast<uintptr_t>(x + start) & 15u) == 0);
     const VT* xv = reinterpret_cast<const VT*>(x + start) + t;
@@ -313,7 +385,7 @@ template <> struct Unroll<double> { static constexpr int value = TFB_UNROLL_F64;
 #else
 #define TFB_LDG_BOUNDS(NT, UF) __launch_bounds__(NT)
 #endif
-template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1>
+template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1, int MS = 0>
 __global__ void TFB_LDG_BOUNDS(NT, UF) leaves_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy,
     int64_t rows, int64_t cols, int leaf_log2, int64_t P,
@@ -337,7 +409,7 @@ __global__ void TFB_LDG_BOUNDS(NT, UF) leaves_kernel(
     const int part = static_cast<int>(rem - l * S);
     const T* xr = x + r * ldx;
     const T* yr = DOT ? y + r * ldy : nullptr;
-    Pair<A> st = leaf_chain<M, T, DOT, VEC, Unroll<T>::value * UF>(
+    Pair<A> st = leaf_chain<M, T, DOT, VEC, Unroll<T>::value * UF, MS>(
         xr, yr, l << leaf_log2, cols, R, part * NT + static_cast<int>(threadIdx.x));
     st = block_tree<M, A>(st, smem, NT);
     if (!fused) {
@@ -749,25 +821,51 @@ static int launch_rows_short(const T* px, const T* py, int64_t ldx, int64_t ldy,
   return check_launch();
 }
 
-template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1>
+template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1, int MS = 0>
 static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                             int leaf_log2, int64_t P, void* partials, void* counters, void* out, int fused,
                             cudaStream_t stream, int64_t part_cap = INT64_MAX) {
   using A = typename Acc<M, T>::type;
-  const void* fn = reinterpret_cast<const void*>(&leaves_kernel<M, T, DOT, VEC, NT, UF>);
+  const void* fn = reinterpret_cast<const void*>(&leaves_kernel<M, T, DOT, VEC, NT, UF, MS>);
   const int64_t units = rows * P * (kThreads / NT);
   const int64_t slots = static_cast<int64_t>(device_sms()) * occupancy_of(fn, NT);
   const int64_t grid64 = units < slots ? units : slots;
   const unsigned grid = static_cast<unsigned>(grid64 > 0 ? grid64 : 1);
   snprintf(g_last_launch, sizeof(g_last_launch),
            "leaves_kernel<%s,%s,%s,%s,NT=%d,U=%d> grid=%u block=%d units=%lld leaf_log2=%d", method_tag(M),
-           sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", VEC ? "ldg128" : "scalar", NT,
-           Unroll<T>::value * UF, grid, NT,
-           static_cast<long long>(units), leaf_log2);
-  leaves_kernel<M, T, DOT, VEC, NT, UF><<<grid, NT, 0, stream>>>(
+           sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum",
+           VEC ? "ldg128" : (MS ? (MS == 1 ? "ldg128-shift1" : MS == 2 ? "ldg128-shift2" : "ldg128-shift3") : "scalar"),
+           NT, Unroll<T>::value * UF, grid, NT, static_cast<long long>(units), leaf_log2);
+  leaves_kernel<M, T, DOT, VEC, NT, UF, MS><<<grid, NT, 0, stream>>>(
       px, py, ldx, ldy, rows, cols, leaf_log2, P, static_cast<Pair<A>*>(partials),
       static_cast<unsigned*>(counters), static_cast<Pair<A>*>(out), fused, part_cap);
   return check_launch();
+}
+
+// Scalar-path (not 16-byte aligned) 256-thread launch: operands that share their
+// offset modulo 16 bytes (1-D, or rows whose pitch is a multiple of 16 bytes)
+// take the shifted-vector loads (leaf_chain, MS > 0), the rest element loads.
+template <int M, typename T, bool DOT>
+static int launch_leaves_unaligned(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
+                                   int leaf_log2, int64_t P, void* partials, void* counters, void* out, int fused,
+                                   cudaStream_t stream, int64_t part_cap) {
+  const uintptr_t mx = reinterpret_cast<uintptr_t>(px) & 15u;
+  const bool pitch_ok = rows == 1 || ((ldx * int64_t(sizeof(T))) % 16 == 0 &&
+                                      (!DOT || (ldy * int64_t(sizeof(T))) % 16 == 0));
+  const bool same = !DOT || (reinterpret_cast<uintptr_t>(py) & 15u) == mx;
+  // binary32 only: the binary64 variant needs 70 registers (3 CTAs/SM) and measured no
+  // faster than element loads (f64 dot 2^27 at offset 1: 338 vs 339-455 us)
+  const int ms = (sizeof(T) == 4 && pitch_ok && same && mx % sizeof(T) == 0) ? static_cast<int>(mx / sizeof(T)) : 0;
+#define TFB_UNAL(MSV)                                                                                       \
+  launch_leaves_nt<M, T, DOT, false, 256, 1, MSV>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, \
+                                                   counters, out, fused, stream, part_cap)
+  if constexpr (sizeof(T) == 4) {
+    if (ms == 1) return TFB_UNAL(1);
+    if (ms == 2) return TFB_UNAL(2);
+    if (ms == 3) return TFB_UNAL(3);
+  }
+  return TFB_UNAL(0);
+#undef TFB_UNAL
 }
 
 template <int M, typename T, bool DOT>
@@ -873,8 +971,8 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
                                                                   partial_capacity);
     else rc = (vec ? launch_leaves_nt<M, T, DOT, true, 256>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,
                                                              nullptr, nullptr, 0, stream, partial_capacity)
-                   : launch_leaves_nt<M, T, DOT, false, 256>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,
-                                                              nullptr, nullptr, 0, stream, partial_capacity));
+                   : launch_leaves_unaligned<M, T, DOT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials,
+                                                         nullptr, nullptr, 0, stream, partial_capacity));
     if (rc) return rc;
     return launch_rows_tree_pdl<M, typename Acc<M, T>::type>(partials, rows, P * S, out, stream, partial_capacity,
                                                              peer, epoch);
@@ -884,6 +982,9 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
   if (deep)
     return launch_leaves_nt<M, T, DOT, true, 256, 2>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters,
                                                      out, fused, stream, cap);
+  if (!vec)
+    return launch_leaves_unaligned<M, T, DOT>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, counters, out,
+                                              fused, stream, cap);
   return TFB_NT(256);
 #undef TFB_NT
 }

@@ -22,7 +22,7 @@ def main():
         R = max(2, -(-(4 * 126 * 10**6) // nbytes))
         bufs = [(torch.rand(n + 4, dtype=dt, device="cuda"), torch.rand(n + 4, dtype=dt, device="cuda"))
                 for _ in range(R)]
-        for off in (0, 1):
+        for off in ((0, 1, 2, 3) if dt == torch.float32 else (0, 1)):
             us = graph_us(lambda i: tfb.reduce(M, bufs[i % R][0][off:off + n], bufs[i % R][1][off:off + n]),
                           max(R, 10))
             print(f"{str(dt)[6:]} dot 2^{lg} offset {off}: {us:9.2f} us {nbytes / us / 1e3:7.0f} GB/s "

@@ -187,6 +187,46 @@ def test_rows_equal_per_row_reduce_and_emulator(tfb, oracle, cuda):
                 _same(got[r], tfb.reduce(meth, X[r], Y[r], leaf_log2=lg).cpu().numpy(), ("row vs 1-D", r))
 
 
+def test_misaligned_binary32_shifted_loads(tfb, oracle, cuda):
+    """binary32 operands 1..3 elements past a 16-byte boundary (shared offset) take the
+    shifted-vector loads (aligned LDG + one lane shuffle; lane 31 reads the next warp's
+    elements): bit-identical to the emulator for every method x sum/dot x TwoProduct, full
+    and partial leaves, explicit leaf sizes, and rows whose pitch keeps the offset."""
+    L = tfb._lib.lib()
+    for n in (4096 * 3 + 5, 100_003, (1 << 20) + 77):
+        xh = oracle.lcg_fill("mmix", n + 8, 81, np.float32, True)
+        yh = oracle.lcg_fill("nr", n + 8, 82, np.float32, True)
+        xd, yd = torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda)
+        for off in (1, 2, 3):
+            x, y = xd[off:off + n], yd[off:off + n]
+            xs, ys = xh[off:off + n], yh[off:off + n]
+            cases = [(m, list(tfb.Method)[m], False) for m in (0, 1, 2, 3, 4)]
+            cases += [(5, tfb.Method.TWOFOLD_FAST, True), (6, tfb.Method.TWOFOLD_RIGOROUS, True)]
+            for m, meth, tp in cases:
+                for yy, yyh in ((None, None), (y, ys)):
+                    if tp and yy is None:
+                        continue
+                    for lg in (0, 12):
+                        got = tfb.reduce(meth, x, yy, leaf_log2=lg, track_product=tp).cpu().numpy()
+                        if lg == 0 and n > 100_000:
+                            assert f"shift{off}" in L.tf_last_launch().decode(), L.tf_last_launch().decode()
+                        _same(got, oracle.emulate(m, xs, yyh, lg), (n, off, m, tp, yy is None, lg))
+    # rows: pitch 4100 floats (16-byte multiple), base 2 elements in -> every row shifted by 2
+    base = torch.from_numpy(oracle.lcg_fill("mmix", 40 * 4100 + 8, 83, np.float32, True)).to(cuda)
+    X = base[2:2 + 40 * 4100].view(40, 4100)[:, :4099]
+    Xh = np.ascontiguousarray(X.cpu().numpy())
+    for m in (2, 3, 4):
+        L.tf_set_rows_kernel(1)
+        try:
+            got = tfb.reduce_rows(list(tfb.Method)[m], X, leaf_log2=10).cpu().numpy()
+            assert "shift2" in L.tf_last_launch().decode(), L.tf_last_launch().decode()
+        finally:
+            L.tf_set_rows_kernel(0)
+        ev, ee = oracle.emulate_rows(m, Xh, None, 10)
+        for r in range(40):
+            _same(got[r], (ev[r], ee[r]), ("rows", m, r))
+
+
 SHORT_COLS = [1, 3, 4, 7, 16, 31, 33, 64, 100, 128, 255, 256, 257, 1000, 1024, 1025, 2049, 4095, 4096]
 
 
