@@ -340,6 +340,31 @@ __device__ __forceinline__ Pair<typename Acc<M, T>::type> leaf_chain(
         else accumulate<M, T, false>(st, vget(a, j), T(0));
       }
     }
+  } else if (!VEC && start + L <= n) {
+    // full leaf, operands not 16-byte aligned: element loads, but U vectors' worth
+    // per operand in flight before the recurrence consumes them (same order)
+    constexpr int UE = U > 2 ? U / 2 : U;
+    int k = 0;
+    for (; k + UE <= R; k += UE) {
+      T a[UE][V], b[UE][V];
+#pragma unroll
+      for (int u = 0; u < UE; ++u)
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          const int64_t i = start + (static_cast<int64_t>(k + u) * kThreads + t) * V + j;
+          a[u][j] = __ldg(x + i);
+          if constexpr (DOT) b[u][j] = __ldg(y + i);
+        }
+#pragma unroll
+      for (int u = 0; u < UE; ++u)
+#pragma unroll
+        for (int j = 0; j < V; ++j) accumulate<M, T, DOT>(st, a[u][j], DOT ? b[u][j] : T(0));
+    }
+    for (; k < R; ++k) {
+      const int64_t base = start + (static_cast<int64_t>(k) * kThreads + t) * V;
+#pragma unroll
+      for (int j = 0; j < V; ++j) accumulate<M, T, DOT>(st, x[base + j], DOT ? y[base + j] : T(0));
+    }
   } else {
     for (int k = 0; k < R; ++k) {
       const int64_t base = start + (static_cast<int64_t>(k) * kThreads + t) * V;
@@ -855,6 +880,7 @@ static int launch_leaves_unaligned(const T* px, const T* py, int64_t ldx, int64_
   const bool same = !DOT || (reinterpret_cast<uintptr_t>(py) & 15u) == mx;
   // binary32 only: the binary64 variant needs 70 registers (3 CTAs/SM) and measured no
   // faster than element loads (f64 dot 2^27 at offset 1: 338 vs 339-455 us)
+  // (measured against the batched element loads below: f32 2^24 dot 23.0-25.9 vs 28.1-28.8 us)
   const int ms = (sizeof(T) == 4 && pitch_ok && same && mx % sizeof(T) == 0) ? static_cast<int>(mx / sizeof(T)) : 0;
 #define TFB_UNAL(MSV)                                                                                       \
   launch_leaves_nt<M, T, DOT, false, 256, 1, MSV>(px, py, ldx, ldy, rows, cols, leaf_log2, P, partials, \
