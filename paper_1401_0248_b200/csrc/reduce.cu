@@ -366,7 +366,27 @@ __device__ __forceinline__ Pair<typename Acc<M, T>::type> leaf_chain(
       for (int j = 0; j < V; ++j) accumulate<M, T, DOT>(st, x[base + j], DOT ? y[base + j] : T(0));
     }
   } else {
-    for (int k = 0; k < R; ++k) {
+    // a row's partial last leaf: the k-rows that lie entirely inside the row one
+    // 16-byte vector at a time (aligned rows), then bounds-checked elements
+    int k = 0;
+    if constexpr (VEC) {
+      const int kfull = static_cast<int>((n - start) / (int64_t(kThreads) * V));
+      const VT* xv = reinterpret_cast<const VT*>(x + start) + t;
+      const VT* yv = DOT ? reinterpret_cast<const VT*>(y + start) + t : nullptr;
+#pragma unroll 1
+      for (; k < kfull; ++k) {
+        VT a = ld_stream(xv + static_cast<int64_t>(k) * kThreads);
+        VT b;
+        if constexpr (DOT) b = ld_stream(yv + static_cast<int64_t>(k) * kThreads);
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          if constexpr (DOT) accumulate<M, T, true>(st, vget(a, j), vget(b, j));
+          else accumulate<M, T, false>(st, vget(a, j), T(0));
+        }
+      }
+    }
+#pragma unroll 1
+    for (; k < R; ++k) {
       const int64_t base = start + (static_cast<int64_t>(k) * kThreads + t) * V;
       if (base >= n) break;  // later k only go further right
 #pragma unroll
