@@ -34,6 +34,21 @@ for dt in (torch.float32, torch.float64):
         tfb.exact_sum(x, absolute=True)
     X = tfb.rows_scaled_normal(7, 5000, seed=3, stream=0, dtype=dt)
     tfb.reduce_rows(tfb.Method.TWOFOLD_FAST, X, X)
+    # session 2 paths: lane-group rows (aligned 32-byte, 16-byte, element loads), the
+    # bulk-copy-fed sequential flavors, shifted loads for misaligned binary32 views
+    for rows, cols, off in ((300, 16, 0), (77, 1000, 0), (50, 37, 1), (9, 4100, 2)):
+        base = tfb.philox_fill("uniform_sym", rows * cols + 8, seed=4, stream=0, dtype=dt)
+        Xr = base[off:off + rows * cols].view(rows, cols)
+        for kind in (0, 1, 2):
+            L.tf_set_rows_kernel(kind)
+            tfb.reduce_rows(tfb.Method.TWOFOLD_RIGOROUS, Xr, Xr)
+        L.tf_set_rows_kernel(0)
+    z = tfb.philox_fill("uniform_sym", 70_003, seed=5, stream=0, dtype=dt)
+    for fl in (tfb.Flavor.sequential(), tfb.Flavor.unrolled(4), tfb.Flavor.unrolled(16)):
+        tfb.reduce(tfb.Method.TWOFOLD_FAST, z[1:], z[1:], flavor=fl)
+        tfb.reduce(tfb.Method.KAHAN, z, flavor=fl)
+    for off in (1, 2, 3):
+        tfb.reduce(tfb.Method.TWOFOLD_FAST, z[off:], z[off:])
     tfb.lcg_fill("mmix", 1000, 1, dt, True, offset=5)
     tfb.two_sum(np.ones(100), np.full(100, 2.0 ** -53))
     tfb.merge_pairs(tfb.Method.TWOFOLD_FAST, torch.randn(5, 2, dtype=torch.float64, device="cuda"))
