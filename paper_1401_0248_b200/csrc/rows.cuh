@@ -55,6 +55,17 @@ __device__ __forceinline__ void chain_vec(Pair<typename Acc<M, T>::type>& st, co
   }
 }
 
+// flat[m + i] of a run of elements read m (runtime, < V) before the wanted start;
+// i is a compile-time index after unrolling, so flat stays in registers.
+template <typename T, int N>
+__device__ __forceinline__ T pick_at(const T (&flat)[N], int m, int i) {
+  if constexpr (Vec<T>::V == 2) {
+    return m ? flat[i + 1] : flat[i];
+  } else {
+    return m == 0 ? flat[i] : m == 1 ? flat[i + 1] : m == 2 ? flat[i + 2] : flat[i + 3];
+  }
+}
+
 // VEC: 0 = element loads (misaligned rows), 1 = 16-byte loads (16-byte aligned
 // rows), 2 = 32-byte loads (32-byte aligned rows).  Same elements, same order.
 template <int M, typename T, bool DOT, int VEC>
@@ -139,6 +150,44 @@ __global__ void TFB_RS_BOUNDS rows_short_kernel(
                   if (oo + q < rem) accumulate<M, T, DOT>(ch[cc], xr[e0 + oo + q], DOT ? yr[e0 + oo + q] : T(0));
               }
             }
+          }
+        } else if (sizeof(T) == 4 && rem >= kChains * V) {
+          // misaligned binary32 row (pitch not a multiple of 16 bytes), whole block:
+          // aligned 16-byte loads around it, each element picked at the row's offset m
+          // (per operand; selects, not local memory), two halves of 4 vectors.  (The
+          // binary64 form measured mixed: +18-34 % at 63-255 columns, -30 % at 17,
+          // from the registers it costs every binary64 misaligned row: not used.)
+          const int mx = static_cast<int>((reinterpret_cast<uintptr_t>(xr + e0) & 15u) / sizeof(T));
+          const int my = DOT ? static_cast<int>((reinterpret_cast<uintptr_t>(yr + e0) & 15u) / sizeof(T)) : 0;
+          const VT* xa = reinterpret_cast<const VT*>(xr + e0 - mx);
+          const VT* ya = DOT ? reinterpret_cast<const VT*>(yr + e0 - my) : nullptr;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            VT a[5], b[5];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              a[c] = __ldg(xa + 4 * h + c);
+              if constexpr (DOT) b[c] = __ldg(ya + 4 * h + c);
+            }
+            // the fifth vector only holds elements of this block when the offset is nonzero
+            a[4] = mx ? __ldg(xa + 4 * h + 4) : a[3];
+            if constexpr (DOT) b[4] = my ? __ldg(ya + 4 * h + 4) : b[3];
+            T fa[5 * V], fb[5 * V];
+#pragma unroll
+            for (int w = 0; w < 5; ++w)
+#pragma unroll
+              for (int q = 0; q < V; ++q) {
+                fa[w * V + q] = vget(a[w], q);
+                if constexpr (DOT) fb[w * V + q] = vget(b[w], q);
+              }
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+#pragma unroll
+              for (int q = 0; q < V; ++q) {
+                const T xv = pick_at(fa, mx, c * V + q);
+                if constexpr (DOT) accumulate<M, T, true>(ch[4 * h + c], xv, pick_at(fb, my, c * V + q));
+                else accumulate<M, T, false>(ch[4 * h + c], xv, T(0));
+              }
           }
         } else {
 #pragma unroll

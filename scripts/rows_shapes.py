@@ -13,7 +13,8 @@ from paper_1401_0248_b200 import _lib  # noqa: E402
 from tail_cost import graph_us  # noqa: E402
 
 SHAPES = [(4096, 65536), (16384, 16384), (32768, 8192), (65536, 4096), (262144, 1024), (1 << 20, 256), (1 << 21, 128), (1 << 22, 64),
-          (1 << 23, 32), (1 << 24, 16), (1 << 20, 1000), (100003, 777)]
+          (1 << 23, 32), (1 << 24, 16), (1 << 20, 1000), (100003, 777),
+          (1 << 22, 17), (1 << 20, 63), (262144, 255), (131072, 513)]
 
 
 def main():
