@@ -828,8 +828,9 @@ static int launch_small(const T* px, const T* py, int64_t n, int64_t P, void* ou
 // kernels, 2 = always the short-row kernel.  Identical results; env TFB_ROWS or
 // tf_set_rows_kernel() choose.  Auto (measured, scripts/rows_shapes.py): lane
 // groups for 16-byte aligned rows of <= 16 KiB per operand (5.6-6.3 TB/s from
-// 16 to 4096 f32 columns, where a CTA per row reaches 0.07-5.8) and for
-// misaligned rows of < 256 elements; a CTA per row above (LDG 6.3-6.5 TB/s
+// 16 to 4096 f32 columns, where a CTA per row reaches 0.07-5.8), misaligned
+// binary32 rows of <= 16 KiB and misaligned binary64 rows of < 256 elements; a
+// CTA per row above (LDG 6.3-6.5 TB/s
 // from 16 to 128 KiB rows; the TMA pipeline from 256 KiB rows, cfg4).
 constexpr int64_t kShortRowMaxBytes = int64_t(16) << 10;
 constexpr int64_t kShortRowMaxScalarCols = 256;
@@ -939,8 +940,10 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
   // Many rows of at most one leaf each: a group of lanes per row (rows.cuh).
   if (fused && !peer && rows > 1 && P == 1) {
     const int rk = rows_kernel_choice();
-    if (rk == 2 || (rk == 0 && (vec ? cols * int64_t(sizeof(T)) <= kShortRowMaxBytes
-                                     : cols < kShortRowMaxScalarCols))) {
+    // misaligned pitches: binary32 blocks use aligned loads + selects (as fast as a CTA
+    // per row from 513 columns up), binary64 ones element loads (CTA per row wins >= 256)
+    if (rk == 2 || (rk == 0 && ((vec || sizeof(T) == 4) ? cols * int64_t(sizeof(T)) <= kShortRowMaxBytes
+                                                        : cols < kShortRowMaxScalarCols))) {
       auto a32 = [](const void* p, int64_t ld) {
         return (reinterpret_cast<uintptr_t>(p) & 31u) == 0 && (ld * int64_t(sizeof(T))) % 32 == 0;
       };
