@@ -42,6 +42,7 @@ int main(int argc, char** argv) {
       cudaMalloc(&records, rbytes))
     return 1;
   cudaMemsetAsync(counters, 0, 4 * (ncounters + 1), s);  /* zero once; kernels leave them zero */
+  cudaMemsetAsync(records, 0, rbytes, s);                  /* the exact oracle's accumulator, likewise */
   CK(tf_fill(TF_DIST_UNIFORM_SYM, TF_F64, 4, 0, 0, n, 0, 0, 0, n, x, s));
   CK(tf_fill(TF_DIST_UNIFORM_SYM, TF_F64, 4, 1, 0, n, 0, 0, 0, n, y, s));
   CK(tf_reduce(TF_TWOFOLD_FAST, TF_F64, x, y, n, 0, pair, partials, pbytes, counters, ncounters, s));

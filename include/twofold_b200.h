@@ -247,8 +247,10 @@ int tf_lcg_fill(int kind, int dtype, uint64_t seed, int sym, int64_t offset, int
  * sums |addend| instead.  out2 (device, 2 doubles): hi = fl(S), lo = fl(S - hi).
  * limbs_out (device, optional, 73 int64): S = sum_k limbs[k] 2^(32k-1074) +
  * limbs[72] 2^(32*72-1074), for exact checks.  Non-finite addends give NaN.
- * Scratch: records (tf_exact_workspace bytes) + one zeroed uint32 counter (left
- * zero).  Integer accumulation makes the result independent of the grid. */
+ * Scratch: `records` (tf_exact_workspace bytes: the grid's integer accumulator)
+ * and one uint32 counter, both ZERO on entry and left zero on exit.  *records
+ * reports the grid size.  Integer accumulation makes the result independent of
+ * the grid. */
 #define TF_EXACT_ABS           1
 #define TF_EXACT_TRUE_PRODUCTS 2
 int tf_exact_workspace(int64_t* records, size_t* bytes);

@@ -10,11 +10,13 @@
 //   * the superaccumulator anchors bit 0 at 2^-1074 and stores 32-bit digits
 //     in int64 limbs (carry-save; 2^31 deposits per limb before overflow);
 //   * at the end every thread deposits its expansion, the CTA normalises its
-//     limbs and writes one record; the last CTA sums the records as integers
-//     (exact and order-independent, hence bit-reproducible for any grid),
-//     normalises, and rounds to hi = fl(S), lo = fl(S - hi) (round to nearest
-//     even; the reference's relative_error uses exactly these two leading
-//     components, expansion.py:129-140).
+//     limbs and adds them into a grid accumulator in global memory with integer
+//     atomics (exact and order-independent, hence bit-reproducible for any
+//     grid); the last CTA (retire ticket) reads the total, zeroes the
+//     accumulator, normalises, and rounds to hi = fl(S), lo = fl(S - hi) (round
+//     to nearest even; the reference's relative_error uses exactly these two
+//     leading components, expansion.py:129-140).  (A per-CTA record summed by the
+//     last CTA cost ~100 µs at 592 CTAs; bit-by-bit rounding another ~50 µs.)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -43,13 +45,9 @@ constexpr int kExactMinBlocks = TFB_EXACT_MINB;  // CTAs per SM (register cap) a
 constexpr int kExpK = TFB_EXACT_K;        // per-thread expansion length
 constexpr int kExpN = 1 + TFB_EXACT_DUAL;  // independent expansions per thread (ILP)
 
-// One CTA record: kLimbs normalised digits in [0, 2^32) + a signed top carry,
-// + a non-finite counter.
-struct ExactRecord {
-  long long limb[kLimbs];
-  long long top;
-  long long nonfinite;
-};
+// Grid accumulator (caller scratch, zero on entry, left zero): kLimbs digit sums,
+// the top carry sum and the non-finite count.
+constexpr int kAccWords = kLimbs + 2;
 
 __device__ __noinline__ void deposit(long long* acc, double v) {
   if (v == 0.0) return;
@@ -154,29 +152,38 @@ __device__ void normalise(long long* limb, long long& top) {
 }
 
 // Round the big integer value (sign, magnitude digits) * 2^-1074 to binary64,
-// nearest-even.  mag: kLimbs+2 digits in [0, 2^32).
+// nearest-even.  mag: ndig digits in [0, 2^32).  Word-wise (O(ndig)), not bit
+// by bit: the 53-bit significand is one 64-bit window, sticky a digit scan.
+__device__ __forceinline__ unsigned long long dig(const unsigned long long* mag, int ndig, int i) {
+  return (i >= 0 && i < ndig) ? mag[i] : 0ull;
+}
+// bits [lo, lo + 64) of the magnitude (bits below 0 read as zero)
+__device__ unsigned long long bits64(const unsigned long long* mag, int ndig, int lo) {
+  const int d = lo >= 0 ? lo >> 5 : -((31 - lo) >> 5);  // floor(lo / 32)
+  const int r = lo - 32 * d;                           // 0..31
+  const unsigned __int128 w = static_cast<unsigned __int128>(dig(mag, ndig, d)) |
+                              (static_cast<unsigned __int128>(dig(mag, ndig, d + 1)) << 32) |
+                              (static_cast<unsigned __int128>(dig(mag, ndig, d + 2)) << 64) |
+                              (static_cast<unsigned __int128>(dig(mag, ndig, d + 3)) << 96);
+  return static_cast<unsigned long long>(w >> r);
+}
 __device__ double round_digits(const unsigned long long* mag, int ndig, bool neg) {
   int hd = ndig - 1;
   while (hd >= 0 && mag[hd] == 0) --hd;
   if (hd < 0) return 0.0;
-  const int hb = 63 - __clzll(mag[hd]);      // highest set bit inside digit hd
-  const int p = hd * 32 + hb;                // position of the leading bit
-  auto bit = [&](int q) -> unsigned long long {
-    return q < 0 ? 0ull : (mag[q >> 5] >> (q & 31)) & 1ull;
-  };
+  const int p = hd * 32 + (63 - __clzll(mag[hd]));  // position of the leading bit
   double out;
   if (p < 53) {  // exactly representable: integer < 2^53 times 2^-1074
-    unsigned long long m = 0;
-    for (int q = p; q >= 0; --q) m = (m << 1) | bit(q);
-    out = scalbn(static_cast<double>(m), -1074);
+    out = scalbn(static_cast<double>(bits64(mag, ndig, 0)), -1074);
   } else {
-    unsigned long long m = 0;
-    for (int q = p; q > p - 53; --q) m = (m << 1) | bit(q);
-    const int lsb = p - 52;                  // weight of m's last bit
-    const unsigned long long guard = bit(lsb - 1);
-    bool sticky = false;
-    for (int q = lsb - 2; q >= 0 && !sticky; --q) sticky = bit(q);
-    if (guard && (sticky || (m & 1ull))) ++m;  // may carry to 2^53: still exact in scalbn
+    const int lsb = p - 52;                          // weight of the significand's last bit
+    unsigned long long m = bits64(mag, ndig, lsb) & ((1ull << 53) - 1);
+    const unsigned long long guard = bits64(mag, ndig, lsb - 1) & 1ull;
+    bool sticky = false;                             // any bit below lsb - 1
+    const int se = lsb - 1;                          // sticky range [0, se)
+    for (int k = 0; k < (se >> 5) && !sticky; ++k) sticky = mag[k] != 0;
+    if (!sticky && (se & 31)) sticky = (dig(mag, ndig, se >> 5) & ((1ull << (se & 31)) - 1)) != 0;
+    if (guard && (sticky || (m & 1ull))) ++m;        // may carry to 2^53: still exact in scalbn
     out = scalbn(static_cast<double>(m), lsb - 1074);
   }
   return neg ? -out : out;
@@ -273,13 +280,17 @@ __device__ __noinline__ void finish(long long* tot, double* out, long long* limb
 template <typename T, int MODE, bool ABS>
 __global__ void __launch_bounds__(kExactThreads, kExactMinBlocks) exact_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t n,
-    ExactRecord* __restrict__ records, unsigned* __restrict__ counter, double* __restrict__ out,
+    long long* __restrict__ gacc, unsigned* __restrict__ counter, double* __restrict__ out,
     long long* __restrict__ limbs_out) {
   constexpr bool DOT = MODE != 0;
-  __shared__ long long acc[kLimbs];
+  // one fixed-point accumulator per warp: the end-of-thread deposits of all 256
+  // expansions would otherwise serialise on the same few shared-memory words
+  __shared__ long long accw[kExactThreads / 32][kLimbs];
+  long long* acc = accw[threadIdx.x >> 5];
+  __shared__ long long s_top;
   __shared__ int s_last;
   __shared__ int s_nonfinite;
-  for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) acc[k] = 0;
+  for (int k = threadIdx.x; k < kLimbs * (kExactThreads / 32); k += blockDim.x) (&accw[0][0])[k] = 0;
   if (threadIdx.x == 0) s_nonfinite = 0;
   __syncthreads();
   double a[kExpN][kExpK];
@@ -335,28 +346,35 @@ __global__ void __launch_bounds__(kExactThreads, kExactMinBlocks) exact_kernel(
     for (int i = 0; i < kExpK; ++i) deposit(acc, a[q][i]);
   if (nonfinite) atomicAdd(&s_nonfinite, nonfinite);
   __syncthreads();
+  for (int k = threadIdx.x; k < kLimbs; k += blockDim.x) {  // the CTA's sum of the warp accumulators
+    long long v = 0;
+#pragma unroll
+    for (int w = 0; w < kExactThreads / 32; ++w) v += accw[w][k];
+    accw[0][k] = v;
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     long long top = 0;
-    normalise(acc, top);
-    ExactRecord& rec = records[blockIdx.x];
-    for (int k = 0; k < kLimbs; ++k) rec.limb[k] = acc[k];
-    rec.top = top;
-    rec.nonfinite = s_nonfinite;
-    __threadfence();
-    s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    normalise(accw[0], top);  // digits in [0, 2^32): the grid total stays far below 2^63
+    s_top = top;
   }
+  __syncthreads();
+  // this CTA's digits into the grid accumulator: integer adds, exact and order-free
+  for (int k = threadIdx.x; k < kLimbs + 2; k += blockDim.x) {
+    const long long v = k < kLimbs ? accw[0][k] : (k == kLimbs ? s_top : static_cast<long long>(s_nonfinite));
+    if (v) atomicAdd(reinterpret_cast<unsigned long long*>(&gacc[k]), static_cast<unsigned long long>(v));
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(counter, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  // last CTA: integer sum of all records (thread k owns limb k), then finish
+  // last CTA: read the total, leave the accumulator zero for the next call, finish
   __shared__ long long tot[kLimbs + 2];
   for (int k = threadIdx.x; k < kLimbs + 2; k += blockDim.x) {
-    long long v = 0;
-    for (unsigned b = 0; b < gridDim.x; ++b) {
-      const ExactRecord& rec = records[b];
-      v += k < kLimbs ? __ldcg(&rec.limb[k]) : (k == kLimbs ? __ldcg(&rec.top) : __ldcg(&rec.nonfinite));
-    }
-    tot[k] = v;
+    tot[k] = __ldcg(&gacc[k]);
+    gacc[k] = 0;
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
@@ -374,7 +392,7 @@ int tf_exact_workspace(int64_t* records, size_t* bytes) {
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t g = static_cast<int64_t>(sms) * kExactMinBlocks;
   if (records) *records = g;
-  if (bytes) *bytes = static_cast<size_t>(g) * sizeof(ExactRecord);
+  if (bytes) *bytes = static_cast<size_t>(kAccWords) * sizeof(long long);
   return TF_OK;
 }
 
@@ -391,11 +409,11 @@ int tf_exact(int dtype, const void* x, const void* y, int64_t n, int flags, void
   const int64_t per = (n + kExactThreads - 1) / kExactThreads;
   if (g > per && per > 0) g = per;  // tiny inputs: fewer CTAs
   if (g < 1) g = 1;
-  if (!records || records_bytes < static_cast<size_t>(g) * sizeof(ExactRecord)) return TF_EWORKSPACE;
+  if (!records || records_bytes < static_cast<size_t>(kAccWords) * sizeof(long long)) return TF_EWORKSPACE;
   auto s = static_cast<cudaStream_t>(stream);
   const bool absval = (flags & TF_EXACT_ABS) != 0;
   const dim3 grid(static_cast<unsigned>(g));
-  auto* rec = static_cast<ExactRecord*>(records);
+  auto* rec = static_cast<long long*>(records);
   auto* ctr = static_cast<unsigned*>(counter);
   auto* o = static_cast<double*>(out2);
   auto* lo = static_cast<long long*>(limbs_out);

@@ -57,7 +57,8 @@ class _Ws:
         with self._lock:
             rec = self._bufs.get(key)
             if rec is None or rec[0].numel() < nbytes:
-                rec = (torch.empty(nbytes, dtype=torch.uint8, device=dev), torch.zeros(1, dtype=torch.int32, device=dev))
+                # both zero on the first call; every tf_exact leaves them zero
+                rec = (torch.zeros(nbytes, dtype=torch.uint8, device=dev), torch.zeros(1, dtype=torch.int32, device=dev))
                 self._bufs[key] = rec
             return rec
 
