@@ -44,15 +44,18 @@ template <> struct Vec<double> { using type = double2; static constexpr int V = 
 
 // Streaming 128-bit loads: read-only path, no L1 allocation (each byte is
 // read exactly once).
+#ifndef TFB_LD_HINT
+#define TFB_LD_HINT ".L1::no_allocate.L2::256B"  // tuning builds may override (scripts/build_ld_variants.sh)
+#endif
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
   float4 r;
-  asm("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+  asm("ld.global.nc" TFB_LD_HINT ".v4.f32 {%0,%1,%2,%3}, [%4];"
       : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
   return r;
 }
 __device__ __forceinline__ double2 ld_stream(const double2* p) {
   double2 r;
-  asm("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0,%1}, [%2];"
+  asm("ld.global.nc" TFB_LD_HINT ".v2.f64 {%0,%1}, [%2];"
       : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
