@@ -151,9 +151,8 @@ __device__ void normalise(long long* limb, long long& top) {
   top += carry;
 }
 
-// Round the big integer value (sign, magnitude digits) * 2^-1074 to binary64,
-// nearest-even.  mag: ndig digits in [0, 2^32).  Word-wise (O(ndig)), not bit
-// by bit: the 53-bit significand is one 64-bit window, sticky a digit scan.
+// Digits of a magnitude (kDig words in [0, 2^32), value * 2^-1074): the 53-bit
+// significand is read as one 64-bit window (bits64), not bit by bit.
 __device__ __forceinline__ unsigned long long dig(const unsigned long long* mag, int ndig, int i) {
   return (i >= 0 && i < ndig) ? mag[i] : 0ull;
 }
@@ -167,114 +166,170 @@ __device__ unsigned long long bits64(const unsigned long long* mag, int ndig, in
                               (static_cast<unsigned __int128>(dig(mag, ndig, d + 3)) << 96);
   return static_cast<unsigned long long>(w >> r);
 }
-__device__ double round_digits(const unsigned long long* mag, int ndig, bool neg) {
-  int hd = ndig - 1;
-  while (hd >= 0 && mag[hd] == 0) --hd;
+// ---- the last CTA's finish, by warp 0 (32 lanes; digit arrays in shared memory,
+// slot k owned by lane k % 32): carry propagation in rounds, sign/magnitude and
+// both roundings with ballot scans instead of one thread walking 74 digits
+// (that serial form cost ~17 µs per call).
+
+constexpr int kDig = kLimbs + 2;  // magnitude digits: 72 limbs + the top carry's two
+
+__device__ __forceinline__ int warp_highest_nonzero(const unsigned long long* a, int n) {
+  int best = -1;
+  for (int base = 0; base < n; base += 32) {
+    const int k = base + static_cast<int>(threadIdx.x & 31);
+    const unsigned b = __ballot_sync(0xffffffffu, k < n && a[k] != 0);
+    if (b) best = base + 31 - __clz(b);
+  }
+  return best;
+}
+__device__ __forceinline__ int warp_lowest_nonzero(const unsigned long long* a, int n) {
+  for (int base = 0; base < n; base += 32) {
+    const int k = base + static_cast<int>(threadIdx.x & 31);
+    const unsigned b = __ballot_sync(0xffffffffu, k < n && a[k] != 0);
+    if (b) return base + __ffs(b) - 1;
+  }
+  return n;
+}
+__device__ __forceinline__ bool warp_any_nonzero_below(const unsigned long long* a, int n) {
+  bool any = false;
+  for (int base = 0; base < n; base += 32) {
+    const int k = base + static_cast<int>(threadIdx.x & 31);
+    any |= __any_sync(0xffffffffu, k < n && a[k] != 0);
+  }
+  return any;
+}
+
+// Round mag (kDig digits, warp-visible) * 2^-1074 to binary64, nearest-even; also
+// reports the significand's last-bit weight `lsb` (-1: exact, no remainder) and
+// whether it rounded up.  Uniform across the warp.
+__device__ double round_digits_warp(const unsigned long long* mag, bool neg, int& lsb_out, bool& up) {
+  lsb_out = -1;
+  up = false;
+  const int hd = warp_highest_nonzero(mag, kDig);
   if (hd < 0) return 0.0;
-  const int p = hd * 32 + (63 - __clzll(mag[hd]));  // position of the leading bit
+  const int p = hd * 32 + (63 - __clzll(mag[hd]));
   double out;
   if (p < 53) {  // exactly representable: integer < 2^53 times 2^-1074
-    out = scalbn(static_cast<double>(bits64(mag, ndig, 0)), -1074);
+    out = scalbn(static_cast<double>(bits64(mag, kDig, 0)), -1074);
   } else {
-    const int lsb = p - 52;                          // weight of the significand's last bit
-    unsigned long long m = bits64(mag, ndig, lsb) & ((1ull << 53) - 1);
-    const unsigned long long guard = bits64(mag, ndig, lsb - 1) & 1ull;
-    bool sticky = false;                             // any bit below lsb - 1
-    const int se = lsb - 1;                          // sticky range [0, se)
-    for (int k = 0; k < (se >> 5) && !sticky; ++k) sticky = mag[k] != 0;
-    if (!sticky && (se & 31)) sticky = (dig(mag, ndig, se >> 5) & ((1ull << (se & 31)) - 1)) != 0;
-    if (guard && (sticky || (m & 1ull))) ++m;        // may carry to 2^53: still exact in scalbn
+    const int lsb = p - 52;
+    unsigned long long m = bits64(mag, kDig, lsb) & ((1ull << 53) - 1);
+    const unsigned long long guard = bits64(mag, kDig, lsb - 1) & 1ull;
+    const int se = lsb - 1;  // sticky range [0, se)
+    bool sticky = warp_any_nonzero_below(mag, se >> 5);
+    if (!sticky && (se & 31)) sticky = (dig(mag, kDig, se >> 5) & ((1ull << (se & 31)) - 1)) != 0;
+    if (guard && (sticky || (m & 1ull))) {
+      ++m;  // may carry to 2^53: still exact in scalbn
+      up = true;
+    }
+    lsb_out = lsb;
     out = scalbn(static_cast<double>(m), lsb - 1074);
   }
   return neg ? -out : out;
 }
 
-// Convert normalised (limb, top) to sign + magnitude digits.
-__device__ bool to_magnitude(const long long* limb, long long top, unsigned long long* mag, int ndig) {
-  // value = sum limb_k 2^(32k) + top * 2^(32 kLimbs); top in {.., -1, 0, 1, ..}
-  // put it in two's complement over ndig digits, then negate if negative
-  for (int k = 0; k < ndig; ++k) mag[k] = 0;
-  for (int k = 0; k < kLimbs; ++k) mag[k] = static_cast<unsigned long long>(limb[k]);
-  long long t = top;
-  for (int k = kLimbs; k < ndig; ++k) {
-    mag[k] = static_cast<unsigned long long>(t) & 0xFFFFFFFFull;
-    t >>= 32;
-  }
-  const bool neg = top < 0;
-  if (neg) {  // magnitude = 2^(32 ndig) - value (two's complement negate)
-    unsigned long long borrow = 1;
-    for (int k = 0; k < ndig; ++k) {
-      unsigned long long v = (~mag[k] & 0xFFFFFFFFull) + borrow;
-      mag[k] = v & 0xFFFFFFFFull;
-      borrow = v >> 32;
-    }
-  }
-  return neg;
-}
-
-// One thread: normalise the summed records, round to (hi, lo), emit limbs.
-__device__ __noinline__ void finish(long long* tot, double* out, long long* limbs_out, unsigned* counter) {
+// tot: kLimbs digit sums (>= 0) + top carry sum + non-finite count, in shared memory.
+// mag, rem: kDig-word shared scratch.  Called by all 32 lanes of one warp.
+__device__ void finish_warp(long long* tot, unsigned long long* mag, unsigned long long* rem, double* out,
+                            long long* limbs_out, unsigned* counter) {
+  const int lane = static_cast<int>(threadIdx.x & 31);
+  __shared__ long long s_carry_top;
   long long top = tot[kLimbs];
   const long long nonfin = tot[kLimbs + 1];
-  normalise(tot, top);
-  constexpr int kDig = kLimbs + 2;
-  unsigned long long mag[kDig];
-  const bool neg = to_magnitude(tot, top, mag, kDig);
+  // normalise: digits to [0, 2^32) in rounds (the first moves < 2^10 per digit, later
+  // rounds only ripple through all-ones digits)
+  for (;;) {
+    long long c[3];
+#pragma unroll
+    for (int sl = 0; sl < 3; ++sl) {
+      const int k = lane + 32 * sl;
+      c[sl] = 0;
+      if (k < kLimbs) {
+        c[sl] = tot[k] >> 32;  // tot[k] >= 0
+        tot[k] &= 0xFFFFFFFFll;
+      }
+    }
+    if (lane == 0) s_carry_top = 0;
+    __syncwarp();
+#pragma unroll
+    for (int sl = 0; sl < 3; ++sl) {
+      const int k = lane + 32 * sl;
+      if (k < kLimbs && c[sl]) {
+        if (k + 1 < kLimbs) tot[k + 1] += c[sl];
+        else s_carry_top = c[sl];
+      }
+    }
+    const bool more = __any_sync(0xffffffffu, (c[0] | c[1] | c[2]) != 0);
+    __syncwarp();
+    top += s_carry_top;
+    __syncwarp();
+    if (!more) break;
+  }
   if (limbs_out) {
-    for (int k = 0; k < kLimbs; ++k) limbs_out[k] = tot[k];
-    limbs_out[kLimbs] = top;
+    for (int k = lane; k < kLimbs; k += 32) limbs_out[k] = tot[k];
+    if (lane == 0) limbs_out[kLimbs] = top;
   }
+  // sign and magnitude: value = D + top * 2^(32 kLimbs), 0 <= D < 2^(32 kLimbs)
+  const bool neg = top < 0;
+  for (int k = lane; k < kLimbs; k += 32) mag[k] = static_cast<unsigned long long>(tot[k]);
+  __syncwarp();
+  unsigned long long utop = static_cast<unsigned long long>(top);
+  if (neg) {  // |value| = (|top| - 1) 2^(32 kLimbs) + (2^(32 kLimbs) - D), or |top| 2^(32 kLimbs) if D = 0
+    const int z = warp_lowest_nonzero(mag, kLimbs);
+    __syncwarp();
+    for (int k = lane; k < kLimbs; k += 32)
+      mag[k] = k < z ? 0ull : (k == z ? (1ull << 32) - mag[k] : 0xFFFFFFFFull - mag[k]);
+    utop = static_cast<unsigned long long>(-top) - (z < kLimbs ? 1ull : 0ull);
+  }
+  if (lane == 0) {
+    mag[kLimbs] = utop & 0xFFFFFFFFull;
+    mag[kLimbs + 1] = utop >> 32;
+  }
+  __syncwarp();
   if (nonfin) {
-    out[0] = __longlong_as_double(0x7FF8000000000000ll);
-    out[1] = out[0];
-    *counter = 0u;
+    if (lane == 0) {
+      out[0] = __longlong_as_double(0x7FF8000000000000ll);
+      out[1] = out[0];
+      *counter = 0u;
+    }
     return;
   }
-  const double hi = round_digits(mag, kDig, neg);
-  if (!isfinite(hi)) {  // |S| beyond binary64: hi = +-inf, no meaningful remainder
-    out[0] = hi;
-    out[1] = 0.0;
-    *counter = 0u;
+  int lsb;
+  bool up;
+  const double hi = round_digits_warp(mag, neg, lsb, up);
+  if (!isfinite(hi) || lsb < 0) {  // beyond binary64 (no meaningful remainder) or exact
+    if (lane == 0) {
+      out[0] = hi;
+      out[1] = 0.0;
+      *counter = 0u;
+    }
     return;
   }
-  // lo = fl(S - hi): subtract |hi| from the magnitude (same sign), round the rest
-  unsigned long long rem[kDig];
-  for (int k = 0; k < kDig; ++k) rem[k] = mag[k];
+  // lo = fl(S - hi).  |S| = m0 2^lsb + low (m0 the truncated significand); hi took
+  // m0 or m0 + 1, so S - hi = +-low or -+(2^lsb - low), 0 < low < 2^lsb when rounded up.
+  const int q = lsb >> 5, qb = lsb & 31;
+  for (int k = lane; k < kDig; k += 32)
+    rem[k] = k < q ? mag[k] : (k == q && qb ? (mag[k] & ((1ull << qb) - 1)) : 0ull);
+  __syncwarp();
   bool rneg = neg;
-  if (hi != 0.0) {
-    // digits of |hi| * 2^1074
-    unsigned long long hd[kDig];
-    for (int k = 0; k < kDig; ++k) hd[k] = 0;
-    const unsigned long long bits = __double_as_longlong(fabs(hi));
-    const int eb = static_cast<int>(bits >> 52);
-    unsigned long long m = bits & 0xFFFFFFFFFFFFFull;
-    int s = 0;
-    if (eb) { m |= 1ull << 52; s = eb - 1; }
-    const int d = s >> 5, r = s & 31;
-    const unsigned long long lo = m << r, hh = r ? (m >> (64 - r)) : 0ull;
-    if (d < kDig) hd[d] = lo & 0xFFFFFFFFull;
-    if (d + 1 < kDig) hd[d + 1] = lo >> 32;
-    if (d + 2 < kDig) hd[d + 2] = hh;
-    // rem = mag - hd (may go negative: then rem = hd - mag with flipped sign)
-    bool ge = true;
-    for (int k = kDig - 1; k >= 0; --k) {
-      if (rem[k] != hd[k]) { ge = rem[k] > hd[k]; break; }
+  if (up) {  // 2^lsb - low, complemented within lsb bits
+    const int z = warp_lowest_nonzero(rem, kDig);
+    __syncwarp();
+    for (int k = lane; k < kDig; k += 32) {
+      const unsigned long long full = k < q ? 0xFFFFFFFFull : (k == q && qb ? (1ull << qb) - 1 : 0ull);
+      rem[k] = k < z ? 0ull : (k == z ? full + 1 - rem[k] : full - rem[k]);
     }
-    const unsigned long long* A = ge ? rem : hd;
-    const unsigned long long* B = ge ? hd : rem;
-    unsigned long long diff[kDig];
-    long long borrow = 0;
-    for (int k = 0; k < kDig; ++k) {
-      long long v = static_cast<long long>(A[k]) - static_cast<long long>(B[k]) - borrow;
-      borrow = v < 0;
-      diff[k] = static_cast<unsigned long long>(v + (borrow << 32)) & 0xFFFFFFFFull;
-    }
-    for (int k = 0; k < kDig; ++k) rem[k] = diff[k];
-    rneg = ge ? neg : !neg;
+    rneg = !neg;
+    __syncwarp();
   }
-  out[0] = hi;
-  out[1] = hi != 0.0 ? round_digits(rem, kDig, rneg) : 0.0;
-  *counter = 0u;  // leave the workspace reusable
+  int lsb2;
+  bool up2;
+  const double lo = round_digits_warp(rem, rneg, lsb2, up2);
+  if (lane == 0) {
+    out[0] = hi;
+    out[1] = lo;
+    *counter = 0u;  // leave the workspace reusable
+  }
 }
 
 template <typename T, int MODE, bool ABS>
@@ -372,13 +427,14 @@ __global__ void __launch_bounds__(kExactThreads, kExactMinBlocks) exact_kernel(
   __threadfence();
   // last CTA: read the total, leave the accumulator zero for the next call, finish
   __shared__ long long tot[kLimbs + 2];
+  __shared__ unsigned long long mag[kDig], rem[kDig];
   for (int k = threadIdx.x; k < kLimbs + 2; k += blockDim.x) {
     tot[k] = __ldcg(&gacc[k]);
     gacc[k] = 0;
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  finish(tot, out, limbs_out, counter);
+  if (threadIdx.x >= 32) return;
+  finish_warp(tot, mag, rem, out, limbs_out, counter);
 }
 
 }  // namespace tfb
