@@ -856,16 +856,18 @@ static int launch_rows_short(const T* px, const T* py, int64_t ldx, int64_t ldy,
   const int g_log2 = rows_short_glog2(cols, V);
   const int64_t K = (cols + int64_t(kThreads) * V - 1) / (int64_t(kThreads) * V);
   TFB_CHECK(K <= (int64_t(1) << leaf_log2) / (int64_t(kThreads) * V));
-  const int64_t rows_per_cta = int64_t(kWarps) * (32 >> g_log2);
+  constexpr int kBlock = TFB_RS_BLOCK;
+  const int64_t rows_per_cta = int64_t(kBlock / 32) * (32 >> g_log2);
   const int64_t want = (rows + rows_per_cta - 1) / rows_per_cta;
-  const int64_t slots = static_cast<int64_t>(device_sms()) * occupancy_of(reinterpret_cast<const void*>(kern));
+  const int64_t slots =
+      static_cast<int64_t>(device_sms()) * occupancy_of(reinterpret_cast<const void*>(kern), kBlock);
   const unsigned grid = static_cast<unsigned>(want < slots ? want : slots);
   snprintf(g_last_launch, sizeof(g_last_launch),
            "rows_short_kernel<%s,%s,%s,%s> grid=%u block=%d rows=%lld cols=%lld lanes/row=%d leaf_log2=%d",
            method_tag(M), sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum",
-           VEC == 2 ? "ldg256" : VEC == 1 ? "ldg128" : "scalar", grid, kThreads, static_cast<long long>(rows),
+           VEC == 2 ? "ldg256" : VEC == 1 ? "ldg128" : "scalar", grid, kBlock, static_cast<long long>(rows),
            static_cast<long long>(cols), 1 << g_log2, leaf_log2);
-  kern<<<grid, kThreads, 0, stream>>>(px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2,
+  kern<<<grid, kBlock, 0, stream>>>(px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2,
                                       static_cast<Pair<A>*>(out));
   return check_launch();
 }

@@ -24,6 +24,9 @@ namespace tfb {
 #ifndef TFB_RS_PARTS
 #define TFB_RS_PARTS 0  // batches the lane's 8 vectors per k are loaded in (0 = f32: 2, f64: 1; measured)
 #endif
+#ifndef TFB_RS_BLOCK
+#define TFB_RS_BLOCK 256  // threads per CTA (any multiple of 32 up to 256)
+#endif
 #if TFB_RS_MINB > 0
 #define TFB_RS_BOUNDS __launch_bounds__(kThreads, TFB_RS_MINB)
 #else
