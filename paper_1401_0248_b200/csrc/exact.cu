@@ -36,7 +36,7 @@ constexpr int kLimbs = 72;   // 72 * 32 = 2304 bit positions >= 2098 + 64 carry 
 #define TFB_EXACT_DUAL 0
 #endif
 #ifndef TFB_EXACT_U
-#define TFB_EXACT_U 2  // 16-byte vectors per operand loaded ahead of the cascades
+#define TFB_EXACT_U 0  // 16-byte vectors per operand loaded ahead of the cascades (0: sums 4, dots 2)
 #endif
 #ifndef TFB_EXACT_MINB
 #define TFB_EXACT_MINB 4
@@ -360,7 +360,9 @@ __global__ void __launch_bounds__(kExactThreads, kExactMinBlocks) exact_kernel(
   // run (the flush atomics keep the compiler from prefetching on its own).
   using VT = typename ExVec<T>::type;
   constexpr int VB = ExVec<T>::V;
-  constexpr int U = TFB_EXACT_U;
+  // measured (scripts/build_exact_variants.sh): sums 4 (f64 2^28 0.589 -> 0.548 ms), dots 2
+  // (f64 dot 2^27 at 4: 0.397 -> 0.440 ms, the second operand's registers)
+  constexpr int U = TFB_EXACT_U > 0 ? TFB_EXACT_U : (DOT ? 2 : 4);
   const bool aligned = (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
                        (!DOT || (reinterpret_cast<uintptr_t>(y) & 15u) == 0);
   int64_t scalar_from = 0;
