@@ -544,6 +544,41 @@ def test_gpu_exact_hard_cases(tfb, oracle, cuda):
     assert tfb.exact_sum(xt[1:]).fraction() == tfb.exact_sum(xt[1:].clone()).fraction()
 
 
+def test_gpu_exact_hi_lo_random_signs_and_scales(tfb, cuda):
+    """The warp-parallel finish (carry rounds, sign/magnitude, both roundings): hi = fl(S)
+    and lo = fl(S - hi) exactly, against Fraction arithmetic, for totals of both signs,
+    exact totals, totals that round up, cancellations to zero and overflow to inf."""
+    from fractions import Fraction
+    rng = np.random.default_rng(11)
+
+    def check(x):
+        want = sum((Fraction(float(v)) for v in x), Fraction(0))
+        got = tfb.exact_sum(x)
+        assert got.fraction() == want
+        if want == 0:
+            assert got.hi == 0.0 and got.lo == 0.0
+            return
+        hi = float(want)  # correctly rounded (Python's Fraction -> float rounds to nearest even)
+        assert got.hi == hi, (x, got)
+        assert got.lo == float(want - Fraction(hi)), (x, got)
+
+    for _ in range(150):
+        m = int(rng.integers(1, 40))
+        x = rng.standard_normal(m) * 2.0 ** rng.integers(-1070, 1000, m)
+        check(x)
+        check(-x)
+        check(np.concatenate([x, -x[: m // 2]]))
+    check(np.array([1.0, -1.0, 2.0 ** -1074, -(2.0 ** -1074)]))  # exact zero
+    check(np.array([2.0 ** 53, 1.0, 1.0]))                         # rounds up, lo negative
+    check(np.array([-(2.0 ** 53), -1.0, -1.0]))
+    check(np.array([2.0 ** 53, 1.0, 2.0 ** -60]))                  # above the tie: rounds up
+    check(np.array([1.5, 2.0 ** -1074]))                           # lo subnormal
+    big = tfb.exact_sum(np.array([1.7e308, 1.7e308]))
+    assert big.hi == np.inf and big.lo == 0.0
+    neg = tfb.exact_sum(np.array([-1.7e308, -1.7e308]))
+    assert neg.hi == -np.inf
+
+
 def test_cfg5_accuracy_at_full_scale_on_gpu(tfb, cuda):
     """BASELINE cfg5 (f64 dottf, N=2^32) is too large for the CPU oracle in a test;
     the GPU exact dot checks the twofold result at full size (64 GiB resident)."""
