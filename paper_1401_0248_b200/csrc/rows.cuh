@@ -154,27 +154,33 @@ __global__ void TFB_RS_BOUNDS rows_short_kernel(
               }
             }
           }
-        } else if (sizeof(T) == 4 && rem >= kChains * V) {
-          // misaligned binary32 row (pitch not a multiple of 16 bytes), whole block:
-          // aligned 16-byte loads around it, each element picked at the row's offset m
-          // (per operand; selects, not local memory), two halves of 4 vectors.  (The
-          // binary64 form measured mixed: +18-34 % at 63-255 columns, -30 % at 17,
-          // from the registers it costs every binary64 misaligned row: not used.)
+        } else if (sizeof(T) == 4 && (rem >= kChains * V || g_log2 > 0)) {
+          // misaligned binary32 row (pitch not a multiple of 16 bytes): aligned 16-byte
+          // loads around the block (only vectors holding a row element: every address
+          // read lies in a 16-byte block of the row), each element picked at the row's
+          // offset m by selects (per operand; not local memory), two halves of 4
+          // vectors; a partial last block is masked element-wise (rows of one lane — at most
+          // 32 elements — measured faster with element loads).  (The binary64 form
+          // measured mixed: +18-34 % at 63-255 columns, -30 % at 17, from the registers
+          // it costs every binary64 misaligned row: not used.)
           const int mx = static_cast<int>((reinterpret_cast<uintptr_t>(xr + e0) & 15u) / sizeof(T));
           const int my = DOT ? static_cast<int>((reinterpret_cast<uintptr_t>(yr + e0) & 15u) / sizeof(T)) : 0;
           const VT* xa = reinterpret_cast<const VT*>(xr + e0 - mx);
           const VT* ya = DOT ? reinterpret_cast<const VT*>(yr + e0 - my) : nullptr;
+          const bool whole = rem >= kChains * V;
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            if (!whole && int64_t(4 * h) * V >= rem) break;
             VT a[5], b[5];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              a[c] = __ldg(xa + 4 * h + c);
-              if constexpr (DOT) b[c] = __ldg(ya + 4 * h + c);
+            for (int w = 0; w < 5; ++w) {
+              const int64_t fx = int64_t(4 * h + w) * V - mx;  // first element of the vector
+              a[w] = (w < 4 || mx) && fx < rem ? __ldg(xa + 4 * h + w) : VT{};
+              if constexpr (DOT) {
+                const int64_t fy = int64_t(4 * h + w) * V - my;
+                b[w] = (w < 4 || my) && fy < rem ? __ldg(ya + 4 * h + w) : VT{};
+              }
             }
-            // the fifth vector only holds elements of this block when the offset is nonzero
-            a[4] = mx ? __ldg(xa + 4 * h + 4) : a[3];
-            if constexpr (DOT) b[4] = my ? __ldg(ya + 4 * h + 4) : b[3];
             T fa[5 * V], fb[5 * V];
 #pragma unroll
             for (int w = 0; w < 5; ++w)
@@ -187,6 +193,7 @@ __global__ void TFB_RS_BOUNDS rows_short_kernel(
             for (int c = 0; c < 4; ++c)
 #pragma unroll
               for (int q = 0; q < V; ++q) {
+                if (!whole && int64_t(4 * h + c) * V + q >= rem) continue;
                 const T xv = pick_at(fa, mx, c * V + q);
                 if constexpr (DOT) accumulate<M, T, true>(ch[4 * h + c], xv, pick_at(fb, my, c * V + q));
                 else accumulate<M, T, false>(ch[4 * h + c], xv, T(0));
