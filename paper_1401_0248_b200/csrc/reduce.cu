@@ -832,11 +832,11 @@ static int launch_small(const T* px, const T* py, int64_t n, int64_t P, void* ou
 // tf_set_rows_kernel() choose.  Auto (measured, scripts/rows_shapes.py): lane
 // groups for 16-byte aligned rows of <= 16 KiB per operand (5.6-6.3 TB/s from
 // 16 to 4096 f32 columns, where a CTA per row reaches 0.07-5.8), misaligned
-// binary32 rows of <= 16 KiB and misaligned binary64 rows of < 256 elements; a
+// binary32 rows of <= 16 KiB and misaligned binary64 rows of < 700 elements; a
 // CTA per row above (LDG 6.3-6.5 TB/s
 // from 16 to 128 KiB rows; the TMA pipeline from 256 KiB rows, cfg4).
 constexpr int64_t kShortRowMaxBytes = int64_t(16) << 10;
-constexpr int64_t kShortRowMaxScalarCols = 256;
+constexpr int64_t kShortRowMaxScalarCols = 700;  // misaligned binary64 (513 columns: 3.45 vs 2.87 TB/s, 777: 3.35 vs 3.74)
 constexpr int64_t kTmaRowMinBytes = int64_t(256) << 10;
 static int g_rows_kernel = -1;
 static int rows_kernel_choice() {
@@ -945,8 +945,8 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
   // Many rows of at most one leaf each: a group of lanes per row (rows.cuh).
   if (fused && !peer && rows > 1 && P == 1) {
     const int rk = rows_kernel_choice();
-    // misaligned pitches: binary32 blocks use aligned loads + selects (as fast as a CTA
-    // per row from 513 columns up), binary64 ones element loads (CTA per row wins >= 256)
+    // misaligned pitches: lane blocks use aligned loads + selects; binary32 up to 16 KiB
+    // rows, binary64 below 700 columns (a CTA per row wins above)
     if (rk == 2 || (rk == 0 && ((vec || sizeof(T) == 4) ? cols * int64_t(sizeof(T)) <= kShortRowMaxBytes
                                                         : cols < kShortRowMaxScalarCols))) {
       auto a32 = [](const void* p, int64_t ld) {

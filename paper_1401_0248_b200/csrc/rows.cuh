@@ -24,6 +24,9 @@ namespace tfb {
 #ifndef TFB_RS_PARTS
 #define TFB_RS_PARTS 0  // batches the lane's 8 vectors per k are loaded in (0 = f32: 2, f64: 1; measured)
 #endif
+#ifndef TFB_RS_SELECT64
+#define TFB_RS_SELECT64 1  // the misaligned select path for binary64 too (measured, profiles/r01_summary.md)
+#endif
 #ifndef TFB_RS_BLOCK
 #define TFB_RS_BLOCK 256  // threads per CTA (any multiple of 32 up to 256)
 #endif
@@ -154,15 +157,14 @@ __global__ void TFB_RS_BOUNDS rows_short_kernel(
               }
             }
           }
-        } else if (sizeof(T) == 4 && (rem >= kChains * V || g_log2 > 0)) {
+        } else if ((sizeof(T) == 4 || TFB_RS_SELECT64) && (rem >= kChains * V || g_log2 > 0)) {
           // misaligned binary32 row (pitch not a multiple of 16 bytes): aligned 16-byte
           // loads around the block (only vectors holding a row element: every address
           // read lies in a 16-byte block of the row), each element picked at the row's
           // offset m by selects (per operand; not local memory), two halves of 4
           // vectors; a partial last block is masked element-wise (rows of one lane — at most
-          // 32 elements — measured faster with element loads).  (The binary64 form
-          // measured mixed: +18-34 % at 63-255 columns, -30 % at 17, from the registers
-          // it costs every binary64 misaligned row: not used.)
+          // 8V elements — measured faster with element loads).  binary64: +54-72 % at 63-255
+          // columns, -17 % at 17 (its registers), kept.
           const int mx = static_cast<int>((reinterpret_cast<uintptr_t>(xr + e0) & 15u) / sizeof(T));
           const int my = DOT ? static_cast<int>((reinterpret_cast<uintptr_t>(yr + e0) & 15u) / sizeof(T)) : 0;
           const VT* xa = reinterpret_cast<const VT*>(xr + e0 - mx);
