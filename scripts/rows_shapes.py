@@ -14,7 +14,7 @@ from tail_cost import graph_us  # noqa: E402
 
 SHAPES = [(4096, 65536), (16384, 16384), (32768, 8192), (65536, 4096), (262144, 1024), (1 << 20, 256), (1 << 21, 128), (1 << 22, 64),
           (1 << 23, 32), (1 << 24, 16), (1 << 20, 1000), (100003, 777),
-          (1 << 22, 17), (1 << 20, 63), (262144, 255), (131072, 513)]
+          (1 << 22, 17), (1 << 20, 63), (262144, 255), (131072, 513), (65536, 5001), (16384, 20001)]
 
 
 def main():
@@ -23,8 +23,11 @@ def main():
     loader = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # 0 = auto, 1 = LDG, 2 = TMA ...
     L.tf_set_loader(loader)
     M = tfb.Method.TWOFOLD_FAST
+    only = [tuple(map(int, a.split("x"))) for a in sys.argv[2:]]  # optional: ROWSxCOLS filters
     for dt in (torch.float32, torch.float64):
         for rows, cols in SHAPES:
+            if only and (rows, cols) not in only:
+                continue
             if dt == torch.float64:
                 rows //= 2
             item = torch.empty(0, dtype=dt).element_size()
