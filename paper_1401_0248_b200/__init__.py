@@ -38,7 +38,7 @@ from .api import (
     two_sum,
     workspace_size,
 )
-from .dist import combine_in_use, peer_combine_error, shard_range, sharded_reduce, sharded_run
+from .dist import combine_in_use, peer_combine_error, rows_range, shard_range, sharded_reduce, sharded_rows, sharded_run
 from .exact import ExactValue, exact_dot, exact_sum, relative_error
 from .gen import CONFIGS, lcg_fill, make_inputs, philox_fill, philox_fill_host, rows_scaled_normal
 
@@ -51,6 +51,7 @@ __all__ = [
     "dot_direct", "dot_wide", "dot_twofold_fast", "dot_twofold_rigorous", "dot_kahan",
     "reduce", "reduce_rows", "sum_rows", "dot_rows", "merge_pairs", "workspace_size", "leaf_log2_for",
     "shard_range", "sharded_reduce", "sharded_run", "combine_in_use", "peer_combine_error",
+    "rows_range", "sharded_rows",
     "ExactValue", "exact_sum", "exact_dot", "relative_error",
     "philox_fill", "philox_fill_host", "lcg_fill", "rows_scaled_normal", "make_inputs", "CONFIGS",
     "__version__",

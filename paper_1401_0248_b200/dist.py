@@ -276,4 +276,51 @@ def sharded_run(method: Method, x_local, y_local=None, *, n_global: int, leaf_lo
     return SumResult(Twofold(t(v), t(0)), n_global)
 
 
-__all__ = ["shard_range", "sharded_reduce", "sharded_run", "peer_combine_error"]
+def rows_range(rows: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous row block [start, stop) of rank `rank` (rows split as evenly as possible)."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    return (rank * rows) // world, ((rank + 1) * rows) // world
+
+
+LocalRows = Callable[[Method, torch.Tensor, "torch.Tensor | None", int], torch.Tensor]
+
+
+def sharded_rows(method: Method, X_local, Y_local=None, *, rows_global: int, leaf_log2: int = 0, group=None,
+                 gather: bool = False, local_reduce: LocalRows | None = None,
+                 track_product: bool = False) -> torch.Tensor:
+    """Row-wise reduction of a matrix sharded by rows (rows shard with no
+    collective).  X_local / Y_local: this rank's contiguous row block rows_range(rows_global,
+    rank, world).  Every row is reduced with the WHOLE matrix's leaf size, so each row's pair
+    is bit-identical to reduce_rows on the unsharded matrix.  Returns this rank's (rows, 2)
+    pairs, or with gather=True all rows_global pairs in row order on every rank (one
+    all-gather of the padded blocks)."""
+    from .api import _as_rows, reduce_rows
+    x = _as_rows(X_local)
+    rows_l, cols = x.shape
+    rank, world = _world(group)
+    lo, hi = rows_range(rows_global, rank, world)
+    if rows_l != hi - lo:
+        raise ValueError(f"X_local has {rows_l} rows; rank {rank} of {world} owns rows [{lo}, {hi})")
+    lg = leaf_log2 or leaf_log2_for(x.dtype, rows_global * cols)
+    if local_reduce is None:
+        pairs = reduce_rows(method, X_local, Y_local, leaf_log2=lg, track_product=track_product)
+    else:
+        pairs = local_reduce(method, x, None if Y_local is None else _as_rows(Y_local), lg)
+    if not gather or world == 1:
+        return pairs
+    block = -(-rows_global // world)  # padded block: ragged blocks all-gather as equal sizes
+    padded = torch.zeros((block, 2), dtype=pairs.dtype, device=pairs.device)
+    padded[:rows_l] = pairs
+    if padded.is_cuda and dist.get_backend(group) == "nccl":
+        table = torch.empty((world * block, 2), dtype=pairs.dtype, device=pairs.device)
+        dist.all_gather_into_tensor(table, padded, group=group)
+        parts = list(table.split(block))
+    else:
+        parts = [torch.empty_like(padded) for _ in range(world)]
+        dist.all_gather(parts, padded, group=group)
+    return torch.cat([parts[r][: rows_range(rows_global, r, world)[1] - rows_range(rows_global, r, world)[0]]
+                      for r in range(world)], 0)
+
+
+__all__ = ["shard_range", "sharded_reduce", "sharded_run", "peer_combine_error", "rows_range", "sharded_rows"]

@@ -141,3 +141,71 @@ def test_ragged_shards_cover_everything(oracle):
     S, A = oracle.exact(x, y), oracle.abs_sum(x, y)
     pair = results[0]["twofold-rigorous"][0]
     assert oracle.deviation(pair[0], pair[1], S) <= oracle.bound(3, np.float64, n, A)
+
+
+def _rows_worker(rank, world, port, rows, cols, dtype_name, q):
+    sys.path.insert(0, REPO)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    import paper_1401_0248_b200 as tfb
+
+    dt = np.float32 if dtype_name == "f32" else np.float64
+    X = O.lcg_fill("mmix", rows * cols, 27, dt, True).reshape(rows, cols)
+    Y = O.lcg_fill("nr", rows * cols, 28, dt, True).reshape(rows, cols)
+    a, b = tfb.rows_range(rows, rank, world)
+
+    def local(method, xl, yl, leaf):
+        mid = list(tfb.Method).index(method)
+        v, e = O.emulate_rows(mid, xl.numpy(), None if yl is None else yl.numpy(), leaf)
+        t = torch.float64 if method is tfb.Method.WIDE else torch.from_numpy(X[:1]).dtype
+        return torch.stack([torch.from_numpy(np.asarray(v, np.float64)), torch.from_numpy(np.asarray(e, np.float64))],
+                           1).to(t)
+
+    out = {}
+    for method in (tfb.Method.TWOFOLD_FAST, tfb.Method.KAHAN, tfb.Method.DIRECT):
+        full = tfb.sharded_rows(method, torch.from_numpy(X[a:b].copy()), torch.from_numpy(Y[a:b].copy()),
+                                rows_global=rows, gather=True, local_reduce=local)
+        mine = tfb.sharded_rows(method, torch.from_numpy(X[a:b].copy()), None, rows_global=rows, local_reduce=local)
+        out[method.value] = (full.numpy().tolist(), mine.numpy().tolist(), (a, b))
+    try:
+        tfb.sharded_rows(tfb.Method.DIRECT, torch.from_numpy(X[: b - a + 1].copy()), rows_global=rows,
+                         local_reduce=local)
+        out["bad_block"] = "no error"
+    except ValueError:
+        out["bad_block"] = "ValueError"
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,rows,dtype_name", [(2, 37, "f32"), (3, 50, "f64")])
+def test_sharded_rows_gather_equals_unsharded(oracle, world, rows, dtype_name):
+    """Rows sharded by contiguous blocks: each rank's pairs use the whole
+    matrix's leaf size, and the gathered table equals the single-device row reduction."""
+    cols = 3000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rows_worker, args=(r, world, port, rows, cols, dtype_name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    dt = np.float32 if dtype_name == "f32" else np.float64
+    X = oracle.lcg_fill("mmix", rows * cols, 27, dt, True).reshape(rows, cols)
+    Y = oracle.lcg_fill("nr", rows * cols, 28, dt, True).reshape(rows, cols)
+    import paper_1401_0248_b200 as tfb
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    lg = tfb.leaf_log2_for(tdt, rows * cols)
+    for name in ("twofold-fast", "kahan", "direct"):
+        mid = oracle.METHODS.index(name)
+        ev, ee = oracle.emulate_rows(mid, X, Y, lg)
+        sv, se = oracle.emulate_rows(mid, X, None, lg)
+        for r in range(world):
+            full, mine, (a, b) = res[r][name]
+            assert [p[0] for p in full] == [float(v) for v in ev] and [p[1] for p in full] == [float(v) for v in ee]
+            assert [p[0] for p in mine] == [float(v) for v in sv[a:b]]
+        assert res[0]["bad_block"] == "ValueError"

@@ -306,6 +306,23 @@ def test_sequential_flavors_streamed_match_reference_order(tfb, oracle, cuda, dt
                     _same(got, oracle.lanes(m, xs, yyh, k), (dt, n, offx, offy, m, "lanes", k))
 
 
+def test_sharded_rows_single_rank_is_reduce_rows(tfb, oracle, cuda):
+    """dist.sharded_rows at world size 1 (no process group): the device kernels with the whole
+    matrix's leaf size, == reduce_rows == the emulator."""
+    rows, cols = 41, 7000
+    Xh = oracle.lcg_fill("mmix", rows * cols, 91, np.float32, True).reshape(rows, cols)
+    Yh = oracle.lcg_fill("nr", rows * cols, 92, np.float32, True).reshape(rows, cols)
+    X, Y = torch.from_numpy(Xh).to(cuda), torch.from_numpy(Yh).to(cuda)
+    got = tfb.sharded_rows(tfb.Method.TWOFOLD_RIGOROUS, X, Y, rows_global=rows, gather=True).cpu().numpy()
+    ref = tfb.reduce_rows(tfb.Method.TWOFOLD_RIGOROUS, X, Y).cpu().numpy()
+    assert np.array_equal(got.view(np.uint8), ref.view(np.uint8))
+    ev, ee = oracle.emulate_rows(3, Xh, Yh)
+    for r in range(rows):
+        _same(got[r], (ev[r], ee[r]), r)
+    with pytest.raises(ValueError):
+        tfb.sharded_rows(tfb.Method.DIRECT, X[:5], rows_global=rows)
+
+
 def test_rows_strided_leading_dimension(tfb, oracle, cuda):
     base = tfb.rows_scaled_normal(9, 5000, seed=4, stream=0, dtype=torch.float32)
     X = base[:, :4999]  # ld = 5000 > cols: 4-byte misaligned rows -> scalar path
