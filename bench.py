@@ -189,6 +189,30 @@ def cpu_port_rate(method_id, xh, yh, nthreads, budget_s=12.0):
     return n / best / 1e9, best, times, res
 
 
+def cpu_rows_rate(method_id, X, Y, nthreads, budget_s=12.0):
+    """Row-wise CPU baseline with the reference's per-row semantics: the seq recurrence
+    (kernels.py:127-243, the oracle's C port) on every row, rows split over threads."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    rows = X.shape[0]
+    chunks = [((i * rows) // nthreads, ((i + 1) * rows) // nthreads) for i in range(nthreads)]
+
+    def work(c):
+        for r in range(*c):
+            O.seq(method_id, X[r], None if Y is None else Y[r])
+
+    times = []
+    with ThreadPoolExecutor(nthreads) as ex:
+        t_start = time.perf_counter()
+        while len(times) < 3 and (not times or time.perf_counter() - t_start < budget_s):
+            t0 = time.perf_counter()
+            list(ex.map(work, chunks))
+            times.append(time.perf_counter() - t0)
+    best = min(times)
+    return X.size / best / 1e9, best, times
+
+
 # ---------------------------------------------------------------------------
 
 def run_reference(args):
@@ -216,6 +240,30 @@ def run_reference(args):
         xh = O.philox_fill("illcond", n, cfg.seed, 0, 0, dt, total=cfg.n, nthreads=nt)
         yh = None
         sample = f"{n} elements, cfg3 layout from the Philox host twin"
+    elif cfg.op == "rows-dot":  # per-row seq on every row, rows over the host threads
+        rng = np.random.default_rng(cfg.seed)
+        scale = (10.0 ** rng.uniform(-4, 4, (cfg.rows, 1))).astype(dt)
+        X = (rng.standard_normal((cfg.rows, cfg.cols)) * scale).astype(dt)
+        Y = (rng.standard_normal((cfg.rows, cfg.cols)) * scale).astype(dt)
+        for _ in range(args.warmup):
+            cpu_rows_rate(mid, X, Y, nt, budget_s=0.0)
+        rates = [cpu_rows_rate(mid, X, Y, nt, budget_s=0.0)[0] for _ in range(args.steps)]
+        value = float(np.mean(rates))
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * X.size / (value * 1e9), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if dt == np.float32 else "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": workload_desc(args.config, cfg, method, cfg.n, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nt, "kind": "port",
+                             "sample": (f"the full {cfg.rows}x{cfg.cols} matrix per step (numpy N(0,1) rows scaled "
+                                        f"by 10^U[-4,4), the config's distribution); the reference seq recurrence "
+                                        f"(kernels.py:203-214) on every row, rows split over {nt} threads"),
+                             "cpu": cpu_model()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        emit(line)
+        return 0
     else:  # normals have no bit-exact host twin: same shapes/distribution, numpy generator
         rng = np.random.default_rng(cfg.seed)
         xh = rng.standard_normal(n).astype(dt)
@@ -477,6 +525,17 @@ def run_ours(args):
 
     # --- CPU baseline (rank 0, N=1 only) ------------------------------------
     cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and rows:
+        from oracle import oracle as O
+        nt = host_threads()
+        Xs = (xh if not args.no_e2e else x.cpu()).numpy()
+        Ys = None if y is None else (yh if not args.no_e2e else y.cpu()).numpy()
+        mid = O.METHODS.index(method_name)
+        rate, best, times = cpu_rows_rate(mid, Xs, Ys, nt)
+        cpu = {"value": rate, "unit": UNIT, "cores": nt, "kind": "port",
+               "sample": (f"the full {Xs.shape[0]}x{Xs.shape[1]} matrix per run, best of {len(times)}; the "
+                          f"reference seq recurrence (kernels.py:203-214) on every row, rows split over {nt} threads"),
+               "cpu": cpu_model()}
     if rank == 0 and world == 1 and not args.no_cpu and not rows:
         from oracle import oracle as O
         nt = host_threads()
