@@ -41,6 +41,9 @@ constexpr int kLimbs = 72;   // 72 * 32 = 2304 bit positions >= 2098 + 64 carry 
 #ifndef TFB_EXACT_MINB
 #define TFB_EXACT_MINB 4
 #endif
+#ifndef TFB_EXACT_MINB_SUM
+#define TFB_EXACT_MINB_SUM TFB_EXACT_MINB  // sums (one operand) may fit more CTAs per SM
+#endif
 constexpr int kExactMinBlocks = TFB_EXACT_MINB;  // CTAs per SM (register cap) and grid = SMs x this
 constexpr int kExpK = TFB_EXACT_K;        // per-thread expansion length
 constexpr int kExpN = 1 + TFB_EXACT_DUAL;  // independent expansions per thread (ILP)
@@ -333,7 +336,7 @@ __device__ void finish_warp(long long* tot, unsigned long long* mag, unsigned lo
 }
 
 template <typename T, int MODE, bool ABS>
-__global__ void __launch_bounds__(kExactThreads, kExactMinBlocks) exact_kernel(
+__global__ void __launch_bounds__(kExactThreads, MODE == 0 ? TFB_EXACT_MINB_SUM : kExactMinBlocks) exact_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t n,
     long long* __restrict__ gacc, unsigned* __restrict__ counter, double* __restrict__ out,
     long long* __restrict__ limbs_out) {
@@ -464,6 +467,7 @@ int tf_exact(int dtype, const void* x, const void* y, int64_t n, int flags, void
   int64_t g = 0;
   size_t need = 0;
   tf_exact_workspace(&g, &need);
+  if (mode == 0) g = g / kExactMinBlocks * TFB_EXACT_MINB_SUM;  // sums: their own CTAs per SM
   const int64_t per = (n + kExactThreads - 1) / kExactThreads;
   if (g > per && per > 0) g = per;  // tiny inputs: fewer CTAs
   if (g < 1) g = 1;
