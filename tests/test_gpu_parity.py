@@ -902,3 +902,35 @@ def test_host_rows_engine_equals_device_rows(tfb, oracle, cuda):
                     # and through the public API (default engine)
                     got = tfb.reduce_rows(list(tfb.Method)[m], xs, ys).cpu().numpy()
                     assert np.array_equal(got.view(np.uint8), want[m].view(np.uint8)), (dt, rows, cols, "api")
+
+
+def test_non_finite_rows_every_rows_kernel(tfb, oracle, cuda):
+    """inf / -inf / NaN and overflowing entries in row-wise reductions: the lane-group kernel
+    (aligned, 32-byte and misaligned-select loads) and the CTA-per-row kernel propagate them
+    exactly as the emulator's per-row tree (NaN payloads excepted)."""
+    L = tfb._lib.lib()
+    rng = np.random.default_rng(8)
+    try:
+        for dt in (np.float32, np.float64):
+            big = np.finfo(dt).max
+            for rows, cols, pad in ((40, 64, 0), (33, 1000, 0), (29, 63, 1), (17, 300, 3)):
+                ld = cols + pad
+                X = rng.uniform(-1, 1, (rows, ld)).astype(dt)
+                Y = rng.uniform(-1, 1, (rows, ld)).astype(dt)
+                X[1, cols // 2] = np.inf
+                X[2, 0], X[2, cols - 1] = np.inf, -np.inf
+                X[3, cols // 3] = np.nan
+                X[4, :2], Y[4, :2] = big, dt(4)
+                Xd = torch.from_numpy(X).to(cuda)[:, :cols]
+                Yd = torch.from_numpy(Y).to(cuda)[:, :cols]
+                Xh, Yh = np.ascontiguousarray(X[:, :cols]), np.ascontiguousarray(Y[:, :cols])
+                for m in _methods(dt):
+                    meth = list(tfb.Method)[m]
+                    ev, ee = oracle.emulate_rows(m, Xh, Yh)
+                    for kind in (1, 2):
+                        L.tf_set_rows_kernel(kind)
+                        got = tfb.reduce_rows(meth, Xd, Yd).cpu().numpy()
+                        for r in range(rows):
+                            _same_nf(got[r], (ev[r], ee[r]), (dt, rows, cols, pad, m, kind, r))
+    finally:
+        L.tf_set_rows_kernel(0)
