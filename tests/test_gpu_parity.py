@@ -934,3 +934,22 @@ def test_non_finite_rows_every_rows_kernel(tfb, oracle, cuda):
                             _same_nf(got[r], (ev[r], ee[r]), (dt, rows, cols, pad, m, kind, r))
     finally:
         L.tf_set_rows_kernel(0)
+
+
+def test_non_finite_misaligned_views(tfb, oracle, cuda):
+    """Non-finite entries through the misaligned paths (binary32 shifted-vector loads,
+    binary64 batched element loads), vs the emulator (NaN payloads excepted)."""
+    rng = np.random.default_rng(9)
+    for dt in (np.float32, np.float64):
+        n = 300_001
+        for off in (1, 2, 3) if dt == np.float32 else (1,):
+            x = rng.uniform(-1, 1, n + 4).astype(dt)
+            y = rng.uniform(-1, 1, n + 4).astype(dt)
+            x[off + 1000] = np.inf
+            x[off + 200_000] = -np.inf if off % 2 else np.nan
+            xd, yd = torch.from_numpy(x).to(cuda), torch.from_numpy(y).to(cuda)
+            xs, ys = x[off:off + n], y[off:off + n]
+            for m in _methods(dt):
+                meth = list(tfb.Method)[m]
+                got = tfb.reduce(meth, xd[off:off + n], yd[off:off + n]).cpu().numpy()
+                _same_nf(got, oracle.emulate(m, xs, ys), (dt, off, m))
