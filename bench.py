@@ -320,10 +320,18 @@ def run_ours(args):
         n_rank = cfg.n // world
     method = tfb.Method(method_name)
     rows = cfg.op == "rows-dot"
+    # rows under torchrun: contiguous row blocks per rank, no collective (dist.sharded_rows)
+    rows_shard = rows and (world > 1 or args.force_collective)
     n = n_rank or cfg.n
     n_global = n * world if n_rank else n
     offset = rank * n if n_rank else 0
-    x, y = make_inputs(cfg, device=dev, offset=offset, n=n if n_rank else None)
+    if rows_shard:
+        r_lo, r_hi = tfb.rows_range(cfg.rows, rank, world)
+        n, offset, n_global = (r_hi - r_lo) * cfg.cols, r_lo * cfg.cols, cfg.n
+        x, y = make_inputs(cfg, device=dev, offset=offset, n=n)
+    else:
+        x, y = make_inputs(cfg, device=dev, offset=offset, n=n if n_rank else None)
+    total_elems = cfg.n if rows_shard else n * world  # elements all ranks process per step
     torch.cuda.synchronize()
     item = x.element_size()
     bytes_per_step = n * item * (1 if y is None else 2)
@@ -344,7 +352,7 @@ def run_ours(args):
     copies = [(x, y)] + [(x.clone(), None if y is None else y.clone()) for _ in range(R - 1)]
     leaf_arg = args.leaf_log2 or lg
 
-    combine_desc = args.combine
+    combine_desc = "none: contiguous row blocks per rank (dist.sharded_rows)" if rows_shard else args.combine
     if not rows and (world > 1 or args.force_collective):
         acc_dt = torch.float64 if method is tfb.Method.WIDE else x.dtype
         if args.combine == "auto":
@@ -355,6 +363,8 @@ def run_ours(args):
 
     def step(i):
         xi, yi = copies[i % R]
+        if rows_shard:
+            return tfb.sharded_rows(method, xi, yi, rows_global=cfg.rows, leaf_log2=args.leaf_log2)
         if rows:
             return tfb.reduce_rows(method, xi, yi, leaf_log2=args.leaf_log2)
         return tfb.sharded_reduce(method, xi, yi, n_global=n_global if n_rank else n, leaf_log2=leaf_arg,
@@ -421,7 +431,7 @@ def run_ours(args):
     if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     step_ms = t.item() / K_eff
-    value = n * world * K_eff / (t.item() * 1e-3) / 1e9
+    value = total_elems * K_eff / (t.item() * 1e-3) / 1e9
 
     # --- kernel-only timing (roofline of the reduction kernel) ---------------
     kernel_ms = timed(kernel_launch) / K_eff
@@ -473,6 +483,8 @@ def run_ours(args):
         ke = args.e2e_steps or max(3, min(K, 10))
 
         def e2e_step():
+            if rows_shard:
+                return tfb.sharded_rows(method, xh, yh, rows_global=cfg.rows).cpu()
             if rows:
                 r = tfb.dot_rows(method, xh, yh)
                 return r.values.cpu()
@@ -496,7 +508,7 @@ def run_ours(args):
             tw = torch.tensor([wall], dtype=torch.float64, device=dev)
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)
             wall = tw.item()
-        e2e = {"value": n * world * ke / wall / 1e9, "unit": UNIT, "h2d_bytes_per_step": bytes_per_step,
+        e2e = {"value": total_elems * ke / wall / 1e9, "unit": UNIT, "h2d_bytes_per_step": bytes_per_step,
                "d2h_bytes_per_step": 16 if not rows else cfg.rows * item,
                "steps": ke, "ms_per_step": 1e3 * wall / ke,
                "path": (("paper_1401_0248_b200.dot_rows(pinned host matrices) -> C-ABI tf_host_reduce_rows "
@@ -554,7 +566,7 @@ def run_ours(args):
     dtype_name = "f64" if item == 8 else "f32"
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
-        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong" if strong else "weak",
+        "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong" if strong or rows_shard else "weak",
         "vs_baseline": None,
         "dtype": dtype_name, "data": "synthetic",
         "config": dict(workload_desc(args.config, cfg, method_name, n, world),
@@ -564,7 +576,7 @@ def run_ours(args):
                        steps_timing=("CUDA graph replay" if use_graph else "eager launches"),
                        **({"parallelism": f"dp{world}: contiguous shards; cross-rank combine: {combine_desc}"}
                           if world > 1 or args.force_collective else {})),
-        "hbm_gbs": bytes_per_step * world * K_eff / (t.item() * 1e-3) / 1e9,
+        "hbm_gbs": bytes_per_step * total_elems / n * K_eff / (t.item() * 1e-3) / 1e9,
         "steps_timed": K_eff,
         "roofline": roofline, "e2e": e2e, "cpu_baseline": cpu,
         "gpu_launches": int(our_launches),
