@@ -165,10 +165,13 @@ int tf_reduce_rows(int method, int dtype, const void* x, const void* y,
  * balanced merge as tf_merge_tree — one launch instead of reduce + NCCL
  * all-gather + merge; every rank gets the bit-identical global pair.
  * peer_ctx: device pointer to a PeerCtx (csrc/peer.cuh; tf_peer_ctx_size()
- * bytes): {int32 world, int32 rank, int32* error, void* bufs[16] (peer r's
- * [2][world] pair buffer), uint32* flags[16] (peer r's [world] flags, zero at
- * creation), uint64 max_spins}.  epoch: 1, 2, 3, ... identical on all ranks
- * for the same call.  A peer that never arrives sets *error and yields NaN.
+ * bytes): {int32 world, int32 rank, int32* error (2 words), void* bufs[16]
+ * (peer r's [2][world] pair buffer), uint32* flags[16] (peer r's [world]
+ * flags, zero at creation), uint64 timeout_ns}.  epoch: 1, 2, 3, ...
+ * identical on all ranks for the same call.  If some peer's pair has not
+ * arrived within timeout_ns, the call writes NaN, error[1] = bitmask of the
+ * missing ranks and error[0] = epoch (per call, not sticky); the caller
+ * checks error[0] == epoch after the stream completes.
  * Unlike tf_reduce, the partials scratch is required even for a single leaf. */
 int tf_reduce_peer(int method, int dtype, const void* x, const void* y, int64_t n, int leaf_log2,
                    void* out_pair, void* partials, size_t partials_bytes, void* counters,

@@ -7,13 +7,20 @@ Reference surface (pkg/src/twofold): ``Method`` (kernels.py:44-49),
 ``rounding_canary`` (eft.py:28-66).  Same names, argument meaning, result
 types and exceptions.  Every flavor runs on the GPU:
 
-  ``cuda``          the grid reduction (default for the ten wrappers): per-thread
-                    recurrences + deterministic TwoSum trees, HBM-bandwidth bound;
-                    value+error tracks the exact sum like any non-sequential flavor
+  ``cuda``          the grid reduction: per-thread recurrences + deterministic
+                    TwoSum trees, HBM-bandwidth bound; value+error tracks the
+                    exact sum like any non-sequential flavor
   ``seq``           one GPU thread running the reference recurrence left to right:
-                    bit-identical to the reference's sequential kernels
+                    bit-identical to the reference's sequential kernels (the
+                    default of the ten sum_* / dot_* wrappers, as in the reference)
   ``unroll:k/vec:k`` k GPU lanes with the reference's lane merge: bit-identical
                     to the reference's lane kernels
+
+The ten wrappers run ``default_flavor()``: ``seq`` unless changed with
+``set_default_flavor`` / ``using_flavor`` or the environment variable
+``TWOFOLD_B200_FLAVOR`` (e.g. ``cuda``), so ``import paper_1401_0248_b200 as
+twofold`` returns the reference's bits until the caller opts into the grid;
+each wrapper also takes an explicit ``flavor=`` keyword.
 
 Inputs may be numpy arrays / array-likes (copied to the GPU; large host
 arrays are streamed in leaf-aligned chunks overlapped with the reduction) or
@@ -165,6 +172,41 @@ class RowsResult:
 
 _CUDA = Flavor.cuda()
 _SEQ = Flavor.sequential()
+
+
+def _env_flavor() -> Flavor:
+    import os
+    spec = os.environ.get("TWOFOLD_B200_FLAVOR", "").strip()
+    return Flavor.parse(spec) if spec else _SEQ
+
+
+_default_flavor = [_env_flavor()]
+
+
+def default_flavor() -> Flavor:
+    """The flavor the ten sum_* / dot_* wrappers run (process-wide)."""
+    return _default_flavor[0]
+
+
+def set_default_flavor(flavor) -> Flavor:
+    """Set the wrappers' flavor (a Flavor or its CLI text, e.g. "cuda"); returns the previous one.
+    The reference's wrappers are sequential (kernels.py:666-706); "cuda" trades those
+    exact bits for the grid reduction's HBM-bound speed and tree accuracy."""
+    fl = Flavor.parse(flavor) if isinstance(flavor, str) else flavor
+    if not isinstance(fl, Flavor):
+        raise TypeError("flavor must be a Flavor or a flavor string")
+    prev, _default_flavor[0] = _default_flavor[0], fl
+    return prev
+
+
+@contextlib.contextmanager
+def using_flavor(flavor):
+    """Context manager form of set_default_flavor (restores the previous flavor)."""
+    prev = set_default_flavor(flavor)
+    try:
+        yield default_flavor()
+    finally:
+        set_default_flavor(prev)
 
 # ---------------------------------------------------------------------------
 # Input handling (kernels.py:574-584 semantics).
@@ -514,44 +556,53 @@ def raw_sum_kernel(method: Method, flavor: Flavor, dtype):
     return kern, method in _TWOFOLD_METHODS
 
 
-def sum_direct(data) -> SumResult:
-    return run_flavor(Method.DIRECT, _CUDA, data)
+def _fl(flavor) -> Flavor:
+    if flavor is None:
+        return _default_flavor[0]
+    return Flavor.parse(flavor) if isinstance(flavor, str) else flavor
 
 
-def sum_wide(data) -> SumResult:
-    return run_flavor(Method.WIDE, _CUDA, data)
+# The ten reference wrappers (kernels.py:666-706): default_flavor(), i.e. the
+# reference's sequential bits unless the caller opts into the grid.
+
+def sum_direct(data, *, flavor=None) -> SumResult:
+    return run_flavor(Method.DIRECT, _fl(flavor), data)
 
 
-def sum_twofold_fast(data) -> SumResult:
-    return run_flavor(Method.TWOFOLD_FAST, _CUDA, data)
+def sum_wide(data, *, flavor=None) -> SumResult:
+    return run_flavor(Method.WIDE, _fl(flavor), data)
 
 
-def sum_twofold_rigorous(data) -> SumResult:
-    return run_flavor(Method.TWOFOLD_RIGOROUS, _CUDA, data)
+def sum_twofold_fast(data, *, flavor=None) -> SumResult:
+    return run_flavor(Method.TWOFOLD_FAST, _fl(flavor), data)
 
 
-def sum_kahan(data) -> SumResult:
-    return run_flavor(Method.KAHAN, _CUDA, data)
+def sum_twofold_rigorous(data, *, flavor=None) -> SumResult:
+    return run_flavor(Method.TWOFOLD_RIGOROUS, _fl(flavor), data)
 
 
-def dot_direct(a, b) -> SumResult:
-    return run_flavor(Method.DIRECT, _CUDA, a, b)
+def sum_kahan(data, *, flavor=None) -> SumResult:
+    return run_flavor(Method.KAHAN, _fl(flavor), data)
 
 
-def dot_wide(a, b) -> SumResult:
-    return run_flavor(Method.WIDE, _CUDA, a, b)
+def dot_direct(a, b, *, flavor=None) -> SumResult:
+    return run_flavor(Method.DIRECT, _fl(flavor), a, b)
 
 
-def dot_twofold_fast(a, b, *, track_product: bool = False) -> SumResult:
-    return run_flavor(Method.TWOFOLD_FAST, _CUDA, a, b, track_product=track_product)
+def dot_wide(a, b, *, flavor=None) -> SumResult:
+    return run_flavor(Method.WIDE, _fl(flavor), a, b)
 
 
-def dot_twofold_rigorous(a, b, *, track_product: bool = False) -> SumResult:
-    return run_flavor(Method.TWOFOLD_RIGOROUS, _CUDA, a, b, track_product=track_product)
+def dot_twofold_fast(a, b, *, flavor=None, track_product: bool = False) -> SumResult:
+    return run_flavor(Method.TWOFOLD_FAST, _fl(flavor), a, b, track_product=track_product)
 
 
-def dot_kahan(a, b) -> SumResult:
-    return run_flavor(Method.KAHAN, _CUDA, a, b)
+def dot_twofold_rigorous(a, b, *, flavor=None, track_product: bool = False) -> SumResult:
+    return run_flavor(Method.TWOFOLD_RIGOROUS, _fl(flavor), a, b, track_product=track_product)
+
+
+def dot_kahan(a, b, *, flavor=None) -> SumResult:
+    return run_flavor(Method.KAHAN, _fl(flavor), a, b)
 
 
 # ---------------------------------------------------------------------------

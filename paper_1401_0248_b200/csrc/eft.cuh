@@ -47,6 +47,23 @@ template <> struct Base<kRigorousTP> { static constexpr int value = kRigorous; }
 template <int M> __host__ __device__ constexpr bool is_tp() { return M == kFastTP || M == kRigorousTP; }
 
 template <typename T> struct Ar;
+#if TFB_PLAIN_OPS
+// NEGATIVE CONTROL ONLY (canary.cu built into libtfb_canary_unsafe.so): plain
+// operators the compiler is free to contract into FMAs under --use_fast_math.
+// The product library never defines TFB_PLAIN_OPS (tests/test_sass.py).
+template <> struct Ar<float> {
+  static __device__ __forceinline__ float add(float a, float b) { return a + b; }
+  static __device__ __forceinline__ float sub(float a, float b) { return a - b; }
+  static __device__ __forceinline__ float mul(float a, float b) { return a * b; }
+  static __device__ __forceinline__ float fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+};
+template <> struct Ar<double> {
+  static __device__ __forceinline__ double add(double a, double b) { return a + b; }
+  static __device__ __forceinline__ double sub(double a, double b) { return a - b; }
+  static __device__ __forceinline__ double mul(double a, double b) { return a * b; }
+  static __device__ __forceinline__ double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
+};
+#else
 template <> struct Ar<float> {
   static __device__ __forceinline__ float add(float a, float b) { return __fadd_rn(a, b); }
   static __device__ __forceinline__ float sub(float a, float b) { return __fsub_rn(a, b); }
@@ -59,6 +76,7 @@ template <> struct Ar<double> {
   static __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
   static __device__ __forceinline__ double fma(double a, double b, double c) { return __fma_rn(a, b, c); }
 };
+#endif
 
 // (value, error) state.  For KAHAN, `e` holds the pending correction c.
 template <typename A> struct Pair { A s, e; };

@@ -15,8 +15,12 @@
 // into the reduction's last step.  Epoch parity double-buffers the slots: a
 // rank can only reuse parity p two calls later, after every peer has already
 // consumed it (completing call k+1 needs every peer's k+1 publication, which
-// each peer issues only after it finished reading call k).  A spin that
-// exceeds the bound sets *error and yields NaN instead of hanging the GPU.
+// each peer issues only after it finished reading call k).  A wait that
+// exceeds timeout_ns (%globaltimer) stamps error[0] = epoch, ORs the missing
+// ranks into error[1] and yields NaN for THAT call only (the stamp is per
+// epoch, never sticky): the host (dist.py) raises RuntimeError on it, and
+// since the late rank's own peers then time out on it in turn, every rank of
+// the group fails the same call instead of some ranks hanging.
 
 namespace tfb {
 
@@ -25,11 +29,18 @@ constexpr int kMaxPeers = 16;
 struct PeerCtx {
   int32_t world;                  // G <= kMaxPeers
   int32_t rank;
-  int32_t* error;                 // local device flag, set on a spin timeout
+  int32_t* error;                 // local device words: [0] epoch of the last timed-out call,
+                                  // [1] bitmask of the ranks that call never heard from
   void* bufs[kMaxPeers];          // peer r's pair buffer: [2][G] Pair<A>
   uint32_t* flags[kMaxPeers];     // peer r's flags: [G] uint32 (epoch of rank g's last publication)
-  unsigned long long max_spins;   // bound of the wait loop (x ~64 ns)
+  unsigned long long timeout_ns;  // bound of the wait (device %globaltimer nanoseconds)
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -63,21 +74,27 @@ __device__ __noinline__ void peer_finish(Pair<A> root, Pair<A>* out, const PeerC
     __threadfence_system();
     st_release_sys(peer->flags[t] + rank, epoch);
   }
+  __shared__ int missing;
+  if (t == 0) missing = 0;
+  group_sync<BAR, NT>();
   if (t < G) {
     const uint32_t* f = peer->flags[rank] + t;
-    unsigned long long spins = 0;
+    const unsigned long long t0 = global_ns();
     while (static_cast<int32_t>(ld_acquire_sys(f) - epoch) < 0) {
-      if (++spins > peer->max_spins) {
-        atomicExch(peer->error, 1);
+      if (global_ns() - t0 > peer->timeout_ns) {
+        atomicOr(&missing, 1 << t);
         break;
       }
-      __nanosleep(64);
+      __nanosleep(256);
     }
   }
   group_sync<BAR, NT>();
   Pair<A> global = tree_over<M, A, NT, BAR>(static_cast<const Pair<A>*>(peer->bufs[rank]) + parity * G, G, smem);
   if (t == 0) {
-    if (*peer->error) {  // a peer never arrived: poison instead of a silent partial sum
+    if (missing) {  // a peer never arrived: poison this call instead of a silent partial sum
+      peer->error[1] = missing;
+      __threadfence();
+      peer->error[0] = static_cast<int32_t>(epoch);
       global.s = A(__longlong_as_double(0x7FF8000000000000ll));
       global.e = global.s;
     }

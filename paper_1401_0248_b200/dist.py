@@ -15,22 +15,25 @@ The local reducer and the merge are injectable so the plumbing can be
 exercised with gloo on CPU (tests/test_dist_gloo.py); the defaults are the
 CUDA kernels and there is no CPU fallback.
 
-combine="peer" replaces reduce + NCCL all-gather + merge by ONE launch
-(tf_reduce_peer, csrc/peer.cuh): the CTA that builds the shard's root writes
-it into every peer's symmetric-memory buffer over NVLink, waits for the G
-pairs (system-scope release/acquire flags, epoch double-buffered, bounded
-spin) and merges them in-kernel.  combine="auto" (the default) uses it for
-device-resident shards at world size > 1 after a one-time self-check: one
-peer combine on known per-rank data must equal the NCCL all-gather + merge
-bit for bit on every rank (all-reduce MIN of the verdicts, so all ranks pick
-the same path); otherwise — no symmetric memory / P2P, a mismatch, a peer
-timeout — it stays on NCCL and combine_in_use() says why.  On this round's
-single-GPU pool the peer kernel is verified at world size 1 (self-publication
-through the same code); multi-GPU by construction plus the self-check.
+combine="nccl" (the default, the north_star design) is that all-gather
+plus the merge kernel.  combine="peer" replaces reduce + NCCL all-gather +
+merge by ONE launch (tf_reduce_peer, csrc/peer.cuh): the CTA that builds the
+shard's root writes it into every peer's symmetric-memory buffer over
+NVLink, waits for the G pairs (system-scope release/acquire flags, epoch
+double-buffered, bounded wait) and merges them in-kernel.  It is opt-in: on
+this round's single-GPU pool it has only run at world size 1 (self-
+publication through the same code).  A peer that does not arrive within the
+timeout (TFB_PEER_TIMEOUT_S, default the process group's default timeout)
+makes that call raise RuntimeError on the host — never a silent NaN — and
+retires the peer combine for the group (later peer calls raise at once;
+NCCL keeps working), so ranks cannot drift apart.  combine="auto" uses the
+peer path for device-resident shards at world size > 1 after a one-time
+self-check against NCCL on every rank.
 """
 
 from __future__ import annotations
 
+import os
 from typing import Callable
 
 import numpy as np
@@ -70,6 +73,21 @@ def _default_merge(method: Method, pairs: torch.Tensor) -> torch.Tensor:
     return merge_pairs(method, pairs)  # enters pairs.device itself
 
 
+def _peer_timeout_ns() -> int:
+    env = os.environ.get("TFB_PEER_TIMEOUT_S")
+    if env:
+        return int(float(env) * 1e9)
+    try:
+        from torch.distributed.constants import default_pg_timeout
+        return int(default_pg_timeout.total_seconds() * 1e9)
+    except Exception:
+        return 1800 * 10 ** 9
+
+
+class PeerTimeout(RuntimeError):
+    """A fused peer combine did not hear from every rank within the timeout."""
+
+
 class _PeerCombine:
     """Symmetric buffers + device PeerCtx for one (group, device, accumulator dtype)."""
 
@@ -85,10 +103,14 @@ class _PeerCombine:
         if world > self.MAX_PEERS:
             raise ValueError(f"peer combine supports up to {self.MAX_PEERS} ranks")
         self.world, self.rank = world, rank
+        # every rank must be here before the (store-based) rendezvous: one NCCL
+        # collective, bounded by the process group's own timeout
+        ready = torch.ones(1, dtype=torch.int32, device=dev)
+        dist.all_reduce(ready, group=group)
         self.buf = symm.empty(2 * world * 2, dtype=acc, device=dev)      # [2 parities][world] pairs
         self.flags = symm.empty(world, dtype=torch.int32, device=dev)    # epoch of rank g's last publication
         self.flags.zero_()
-        self.error = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.error = torch.zeros(2, dtype=torch.int32, device=dev)       # [epoch of a timeout, missing mask]
         torch.cuda.synchronize(dev)
         pg = group if group is not None else dist.group.WORLD
         hb = symm.rendezvous(self.buf, pg)
@@ -96,16 +118,25 @@ class _PeerCombine:
         dist.barrier(group)
         bufs = list(hb.buffer_ptrs) + [0] * (self.MAX_PEERS - world)
         flags = list(hf.buffer_ptrs) + [0] * (self.MAX_PEERS - world)
-        max_spins = 1 << 27  # x ~64 ns: seconds, then *error = 1 and NaN instead of a hang
-        raw = struct.pack("<iiQ16Q16QQ", world, rank, self.error.data_ptr(), *bufs, *flags, max_spins)
+        raw = struct.pack("<iiQ16Q16QQ", world, rank, self.error.data_ptr(), *bufs, *flags, _peer_timeout_ns())
         assert len(raw) == _lib.lib().tf_peer_ctx_size(), "PeerCtx layout mismatch"
         self.ctx = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev)
         self.epoch = 0
+        self.failed: str | None = None
         self._handles = (hb, hf)  # keep the mappings alive
 
     def next_epoch(self) -> int:
         self.epoch += 1
         return self.epoch
+
+    def check(self, epoch: int, error_words) -> None:
+        """Raise PeerTimeout if call `epoch` timed out; error_words = (stamped epoch, missing mask)."""
+        stamped, missing = int(error_words[0]), int(error_words[1])
+        if stamped == epoch:
+            ranks = [r for r in range(self.world) if (missing >> r) & 1]
+            self.failed = (f"peer combine call {epoch} on rank {self.rank} timed out waiting for rank(s) {ranks}; "
+                           "the peer combine is retired for this group (use combine='nccl')")
+            raise PeerTimeout(self.failed)
 
 
 _peer_cache: dict = {}
@@ -120,24 +151,35 @@ def _peer_combine_for(group, dev: torch.device, acc: torch.dtype) -> _PeerCombin
     return pc
 
 
-def _reduce_peer(method: Method, x: torch.Tensor, y, leaf_log2: int, group, track_product: bool) -> torch.Tensor:
+def _reduce_peer(method: Method, x: torch.Tensor, y, leaf_log2: int, group, track_product: bool,
+                 pc: _PeerCombine | None = None, launch=None) -> torch.Tensor:
+    """One fused reduce + peer combine, then (synchronously) the timeout check.
+    `pc` / `launch` are injectable for the CPU tests of the failure path."""
     from . import _lib
     from .api import _acc_dtype, _dtype_code, _mid, _on_device, _ptr, _scratch, _stream_ptr, workspace_size
     dev = x.device
-    _lib.ensure_canary(dev.index)
-    y = _on_device(y, dev)
-    x = x.contiguous()
     acc = _acc_dtype(method, x.dtype)
-    pc = _peer_combine_for(group, dev, acc)
-    out = torch.empty(2, dtype=acc, device=dev)
-    pb, cnt, _ = workspace_size(method, x.dtype, 1, x.numel(), leaf_log2)
-    parts, ctrs = _scratch.get(dev, pb, cnt)
-    with torch.cuda.device(dev):
-        _lib.check(_lib.lib().tf_reduce_peer(_mid(method, track_product, y is not None), _dtype_code(x.dtype),
-                                             _ptr(x), _ptr(y), x.numel(), leaf_log2, out.data_ptr(), _ptr(parts),
-                                             pb, _ptr(ctrs), cnt, pc.ctx.data_ptr(), pc.next_epoch(),
-                                             _stream_ptr(dev)),
-                   "tf_reduce_peer")
+    if pc is None:
+        _lib.ensure_canary(dev.index)
+        pc = _peer_combine_for(group, dev, acc)
+    if pc.failed:
+        raise PeerTimeout(pc.failed)
+    epoch = pc.next_epoch()
+    if launch is not None:
+        out = launch(pc, epoch)
+    else:
+        y = _on_device(y, dev)
+        x = x.contiguous()
+        out = torch.empty(2, dtype=acc, device=dev)
+        pb, cnt, _ = workspace_size(method, x.dtype, 1, x.numel(), leaf_log2)
+        parts, ctrs = _scratch.get(dev, pb, cnt)
+        with torch.cuda.device(dev):
+            _lib.check(_lib.lib().tf_reduce_peer(_mid(method, track_product, y is not None), _dtype_code(x.dtype),
+                                                 _ptr(x), _ptr(y), x.numel(), leaf_log2, out.data_ptr(),
+                                                 _ptr(parts), pb, _ptr(ctrs), cnt, pc.ctx.data_ptr(), epoch,
+                                                 _stream_ptr(dev)),
+                       "tf_reduce_peer")
+    pc.check(epoch, pc.error.tolist())  # .tolist() waits for the launch
     return out
 
 
@@ -168,8 +210,8 @@ def _peer_self_check(group, dev: torch.device, acc: torch.dtype) -> str | None:
             if not torch.equal(got.view(torch.int64 if dt == torch.float64 else torch.int32),
                                want.view(torch.int64 if dt == torch.float64 else torch.int32)):
                 reason = "peer self-check result differs from the NCCL combine"
-            elif peer_combine_error(group):
-                reason = "peer self-check timed out waiting for a peer"
+    except PeerTimeout as exc:
+        reason = f"peer self-check: {exc}"
     except Exception as exc:  # no symmetric memory / P2P on this box
         reason = f"peer combine unavailable: {type(exc).__name__}: {exc}"
     return _agree(reason, group, dev)
@@ -195,9 +237,12 @@ def combine_in_use(group=None, dev: torch.device | None = None, acc: torch.dtype
     return "peer" if reason is None else f"nccl ({reason})"
 
 
-def peer_combine_error(group=None) -> bool:
-    """True if any peer combine on this rank timed out waiting for a peer (result NaN)."""
-    return any(int(pc.error.item()) != 0 for (gid, _, _), pc in _peer_cache.items() if gid == id(group))
+def peer_combine_error(group=None) -> str | None:
+    """Why the peer combine was retired for this group on this rank (a timeout), else None."""
+    for (gid, _, _), pc in _peer_cache.items():
+        if gid == id(group) and pc.failed:
+            return pc.failed
+    return None
 
 
 def _world(group) -> tuple[int, int]:
@@ -210,15 +255,17 @@ def sharded_reduce(method: Method, x_local: torch.Tensor, y_local: torch.Tensor 
                    n_global: int, leaf_log2: int = 0, group=None,
                    local_reduce: LocalReduce | None = None, merge: Merge | None = None,
                    track_product: bool = False, force_collective: bool = False,
-                   combine: str = "auto") -> torch.Tensor:
+                   combine: str = "nccl") -> torch.Tensor:
     """Raw (value, error) pair of the global array, identical on every rank.
 
     x_local / y_local: this rank's shard (CUDA tensors for the default
     reducer).  leaf_log2 = 0 uses the global array's auto leaf size, so the
     partition does not depend on G.  combine: "peer" (fused NVLink combine
-    inside the reduction launch), "nccl" (all-gather + merge kernel), or
-    "auto" (default: peer for device-resident shards at world size > 1 once a
-    one-time self-check against NCCL passed on every rank, else nccl).
+    inside the reduction launch; synchronous, raises PeerTimeout if a peer
+    never arrives), "nccl" (default: all-gather + merge kernel), or "auto"
+    (peer for device-resident shards at world size > 1 once a one-time
+    self-check against NCCL passed on every rank and no timeout retired it,
+    else nccl).
     """
     if combine not in ("nccl", "peer", "auto"):
         raise ValueError("combine must be 'auto', 'nccl' or 'peer'")
@@ -231,7 +278,8 @@ def sharded_reduce(method: Method, x_local: torch.Tensor, y_local: torch.Tensor 
         combine = "nccl"
         if (distributed and local_reduce is None and merge is None and x_local.is_cuda and not capturing
                 and _world(group)[1] > 1
-                and combine_in_use(group, x_local.device, _acc_dtype(method, x_local.dtype)) == "peer"):
+                and combine_in_use(group, x_local.device, _acc_dtype(method, x_local.dtype)) == "peer"
+                and not peer_combine_error(group)):
             combine = "peer"
     if combine == "peer" and distributed and local_reduce is None:
         if not x_local.is_cuda:
@@ -323,4 +371,5 @@ def sharded_rows(method: Method, X_local, Y_local=None, *, rows_global: int, lea
                       for r in range(world)], 0)
 
 
-__all__ = ["shard_range", "sharded_reduce", "sharded_run", "peer_combine_error", "rows_range", "sharded_rows"]
+__all__ = ["shard_range", "sharded_reduce", "sharded_run", "peer_combine_error", "PeerTimeout", "rows_range",
+           "sharded_rows"]

@@ -1,16 +1,25 @@
 """Exact (correctly rounded) sums and dot products on the GPU.
 
-Device counterpart of the reference's expansion oracle (expansion.py:79-140):
-``exact_sum`` / ``exact_dot`` return the exact value's two leading binary64
-components (hi = fl(S), lo = fl(S - hi)) — exactly what the reference's
-``relative_error`` consumes (``Expansion.hi`` / ``.lo``) — plus the full
-fixed-point representation for rational checks.  Integer superaccumulation
-makes the result independent of grid size and order.
+Device counterpart of the reference's expansion oracle (expansion.py):
+``exact_sum`` / ``exact_dot`` return an ``ExactValue``, an ``Expansion``
+(the reference's non-overlapping component tuple, increasing magnitude, so
+``.components`` / ``.hi`` / ``.lo`` / ``float()`` / ``.add`` work as in
+expansion.py:31-70) that also carries the device superaccumulator's exact
+fixed-point limbs for rational checks.  Integer superaccumulation makes the
+result independent of grid size and order.
+
+Semantics follow expansion.py:112-126: ``exact_dot`` of binary32 data sums
+the exact products (each f32*f32 product is exact in binary64); of binary64
+data, the products rounded once to binary64.  ``rounded_products=True``
+selects the binary32 kernels' own addends fl32(a*b) instead (what the
+grid's error channel tracks), ``true_products=True`` the exact products at
+either precision (what a TwoProduct dot tracks).
 """
 
 from __future__ import annotations
 
 import ctypes
+import math
 import threading
 from dataclasses import dataclass
 from fractions import Fraction
@@ -26,25 +35,91 @@ TF_EXACT_TRUE_PRODUCTS = 2
 _LIMBS = 72
 
 
-@dataclass(frozen=True)
-class ExactValue:
-    """hi = fl(S), lo = fl(S - hi); limbs: S = sum limbs[k] 2^(32k-1074) + limbs[72] 2^(32*72-1074)."""
+def _two_sum(a: float, b: float) -> tuple[float, float]:
+    """Knuth TwoSum on Python floats (binary64), for the host-side expansion
+    bookkeeping of Expansion.add (the reference does the same in Python, eft.py:45-56)."""
+    x = a + b
+    bv = x - a
+    av = x - bv
+    return x, (a - av) + (b - bv)
 
-    hi: float
-    lo: float
-    limbs: tuple
+
+@dataclass(frozen=True)
+class Expansion:
+    """Non-overlapping binary64 expansion, components in increasing magnitude
+    (expansion.py:31-70); the zero expansion has no components."""
+
+    components: tuple
+
+    @property
+    def is_zero(self) -> bool:
+        return not self.components
+
+    @property
+    def hi(self) -> float:
+        """Largest-magnitude component (0.0 for zero)."""
+        return self.components[-1] if self.components else 0.0
+
+    @property
+    def lo(self) -> float:
+        """Second-largest component (0.0 if absent)."""
+        return self.components[-2] if len(self.components) > 1 else 0.0
+
+    def __float__(self) -> float:
+        return math.fsum(self.components)  # correctly rounded sum of the components
+
+    def add(self, v: float) -> "Expansion":
+        """Grow by one finite binary64 value, exactly (a TwoSum cascade)."""
+        q = float(v)
+        out = []
+        for c in self.components:
+            q, r = _two_sum(q, c)
+            if r != 0.0:
+                out.append(r)
+        if q != 0.0:
+            out.append(q)
+        return Expansion(tuple(out))
+
+
+ZERO = Expansion(())
+
+
+def expansion_add(e: Expansion, v: float) -> Expansion:
+    """Functional form of Expansion.add (expansion.py:73-75)."""
+    return e.add(v)
+
+
+def _components_of(q: Fraction) -> tuple:
+    """Nearest-rounding decomposition of an exact rational into a non-overlapping
+    binary64 expansion: c_top = fl(S), c_next = fl(S - c_top), ...  (|remainder|
+    <= ulp/2 each step, so the components do not overlap); increasing magnitude."""
+    comps = []
+    while q != 0 and len(comps) < 64:
+        try:
+            c = float(q)  # correctly rounded (Fraction.__float__ rounds to nearest)
+        except OverflowError:  # |S| beyond binary64: the reference's cascade overflows to inf too
+            return (math.inf if q > 0 else -math.inf,)
+        comps.append(c)
+        q -= Fraction(c)
+    return tuple(reversed(comps))
+
+
+@dataclass(frozen=True)
+class ExactValue(Expansion):
+    """An Expansion computed on the device, plus its exact fixed-point limbs:
+    S = sum limbs[k] 2^(32k-1074) + limbs[72] 2^(32*72-1074)."""
+
+    limbs: tuple = ()
 
     def fraction(self) -> Fraction:
         v = sum(int(c) << (32 * k) for k, c in enumerate(self.limbs[:_LIMBS]))
         v += int(self.limbs[_LIMBS]) << (32 * _LIMBS)
         return Fraction(v, 1 << 1074)
 
-    @property
-    def is_zero(self) -> bool:
-        return self.hi == 0.0
-
-    def __float__(self) -> float:
-        return self.hi
+    @classmethod
+    def from_limbs(cls, limbs: tuple) -> "ExactValue":
+        v = sum(int(c) << (32 * k) for k, c in enumerate(limbs[:_LIMBS])) + (int(limbs[_LIMBS]) << (32 * _LIMBS))
+        return cls(_components_of(Fraction(v, 1 << 1074)), tuple(limbs))
 
 
 class _Ws:
@@ -81,35 +156,46 @@ def _exact(x: torch.Tensor, y: torch.Tensor | None, flags: int) -> ExactValue:
                              flags, out.data_ptr(), limbs.data_ptr(), buf.data_ptr(), nbytes.value,
                              counter.data_ptr(), _stream_ptr(dev)), "tf_exact")
     hi, lo = out.cpu().tolist()
-    return ExactValue(hi, lo, tuple(limbs.cpu().tolist()))
+    ev = ExactValue.from_limbs(tuple(limbs.cpu().tolist()))
+    if math.isfinite(ev.hi) and (ev.hi, ev.lo) != (hi, lo):  # the device's own rounding of the limbs must agree
+        raise RuntimeError(f"tf_exact: leading components ({hi!r}, {lo!r}) disagree with the limbs {ev.components!r}")
+    return ev
 
 
 def exact_sum(data, *, absolute: bool = False) -> ExactValue:
     """Exact sum of a float32/float64 array (expansion.exact_sum, expansion.py:104-109)."""
     x = _as_tensor(data)
     if x.numel() == 0:
-        return ExactValue(0.0, 0.0, (0,) * (_LIMBS + 1))
+        return ExactValue((), (0,) * (_LIMBS + 1))
     return _exact(x, None, TF_EXACT_ABS if absolute else 0)
 
 
-def exact_dot(a, b, *, true_products: bool = False, absolute: bool = False) -> ExactValue:
-    """Exact sum of the products.  Default: the products rounded in the data
-    precision — the identical addends the twofold dot kernels sum (for binary64
-    this is expansion.exact_dot, expansion.py:112-126).  true_products=True:
-    the exact products (what a TwoProduct dot tracks; for binary32 this is the
-    reference's exact_dot)."""
+def exact_dot(a, b, *, rounded_products: bool = False, true_products: bool = False,
+              absolute: bool = False) -> ExactValue:
+    """Exact sum of the elementwise products, as expansion.exact_dot (expansion.py:112-126):
+    binary32 data -> the exact products; binary64 data -> the products rounded once
+    to binary64 (the addends the binary64 dot kernels see).
+
+    rounded_products=True: the products rounded in the DATA precision for either
+    dtype — for binary32 the addends fl32(a*b) the binary32 dot kernels sum, so
+    the grid's error channel is judged against its own addends.
+    true_products=True: the exact products for either dtype (the TwoProduct target).
+    """
+    if rounded_products and true_products:
+        raise ValueError("rounded_products and true_products are exclusive")
     x, y = _as_tensor(a), _as_tensor(b)
     if x.dtype != y.dtype:
         raise TypeError("dot operands must share a dtype")
     if x.shape != y.shape:
         raise ValueError("exact_dot needs equal-length arrays")
     if x.numel() == 0:
-        return ExactValue(0.0, 0.0, (0,) * (_LIMBS + 1))
-    flags = (TF_EXACT_TRUE_PRODUCTS if true_products else 0) | (TF_EXACT_ABS if absolute else 0)
+        return ExactValue((), (0,) * (_LIMBS + 1))
+    exact_products = true_products or (x.dtype == torch.float32 and not rounded_products)
+    flags = (TF_EXACT_TRUE_PRODUCTS if exact_products else 0) | (TF_EXACT_ABS if absolute else 0)
     return _exact(x, y, flags)
 
 
-def relative_error(approx: float, reference: ExactValue) -> float:
+def relative_error(approx: float, reference: Expansion) -> float:
     """(approx - reference) / reference from the two leading components,
     exactly as expansion.relative_error (expansion.py:129-140)."""
     if reference.is_zero:
@@ -118,4 +204,4 @@ def relative_error(approx: float, reference: ExactValue) -> float:
     return ((float(approx) - hi) - lo) / (hi + lo)
 
 
-__all__ = ["ExactValue", "exact_sum", "exact_dot", "relative_error"]
+__all__ = ["Expansion", "ExactValue", "ZERO", "expansion_add", "exact_sum", "exact_dot", "relative_error"]

@@ -31,6 +31,7 @@ from .exact import exact_sum, relative_error
 from .gen import lcg_fill
 
 _CUDA = Flavor.cuda()
+_SEQ = Flavor.sequential()
 _TWOFOLD = (Method.TWOFOLD_FAST, Method.TWOFOLD_RIGOROUS)
 DTYPES = {"f32": torch.float32, "f64": torch.float64}
 TIERS = {"small": 256 << 10, "medium": 32 << 20, "large": 2 << 30}  # bytes per operand
@@ -255,8 +256,10 @@ DEFAULT_METHODS = (Method.DIRECT, Method.KAHAN, Method.TWOFOLD_FAST)
 
 
 def run_accuracy_table(n: int = 1_000_000, seed: int = 1, methods=DEFAULT_METHODS, precisions=("f32", "f64"),
-                       generators=("nr", "mmix"), intervals=("unit", "sym"), flavor: Flavor = _CUDA):
-    """accuracy.run_accuracy_table (accuracy.py:73-103) on the GPU."""
+                       generators=("nr", "mmix"), intervals=("unit", "sym"), flavor: Flavor = _SEQ):
+    """accuracy.run_accuracy_table (accuracy.py:73-103) on the GPU.  Default flavor:
+    seq, the reference's (accuracy.py:97), so the table reproduces its numbers;
+    flavor=Flavor.cuda() scores the grid reduction instead."""
     if n < 1:
         raise ValueError("n must be >= 1")
     rows = []
@@ -301,28 +304,33 @@ def run_hours100(flavor: Flavor = Flavor.sequential()):
     return rows
 
 
-def run_scaling_study(ns=(10 ** 3, 10 ** 4, 10 ** 5, 10 ** 6, 10 ** 7), trials: int = 100, seed: int = 1,
-                      methods=(Method.DIRECT, Method.TWOFOLD_FAST), flavor: Flavor = _CUDA):
-    """Median |relative error| vs N over seeded f32 NR trials, and the fitted
-    log-log slope per method (accuracy.py:139-173 methodology)."""
+def run_scaling_study(ns=(10 ** 3, 10 ** 4, 10 ** 5, 10 ** 6), trials: int = 100, seed: int = 1,
+                      methods=(Method.DIRECT, Method.TWOFOLD_FAST), flavor: Flavor = _SEQ,
+                      generator: str = "nr"):
+    """Median |relative error| vs N over seeded binary32 trials (trial t draws
+    uniform [0,1) data from seed + t) and the fitted log-log slope per method,
+    as accuracy.run_scaling_study (accuracy.py:139-173): direct scored on value,
+    twofold on value + error, no slope for a method with an exact-zero median.
+    Default flavor seq (the reference's, :159)."""
     out = []
+    medians = {m: [] for m in methods}
     for n in ns:
         errs = {m: [] for m in methods}
         for t in range(trials):
-            data = lcg_fill("nr", n, seed + t, torch.float32)
+            data = lcg_fill(generator, n, seed + t, torch.float32)
             ref = exact_sum(data)
             for m in methods:
                 errs[m].append(abs(relative_error(_score(m, run_flavor(m, flavor, data)), ref)))
         for m in methods:
-            out.append((n, m.value, float(np.median(errs[m]))))
+            med = float(np.median(errs[m]))
+            medians[m].append(med)
+            out.append((n, m.value, med))
     slopes = {}
+    logn = np.log10(np.asarray(ns, float))
     for m in methods:
-        pts = [(math.log10(n), math.log10(e)) for n, mv, e in out if mv == m.value and e > 0]
-        if len(pts) >= 2:
-            xs, ys = zip(*pts)
-            slopes[m.value] = float(np.polyfit(xs, ys, 1)[0])
-        else:
-            slopes[m.value] = None
+        med = np.asarray(medians[m])
+        slopes[m.value] = (float(np.polyfit(logn, np.log10(med), 1)[0])
+                           if len(ns) >= 2 and np.all(med > 0) else None)
     return out, slopes
 
 

@@ -132,6 +132,69 @@ def test_auto_combine_decision_is_collective():
     assert res[0][1] == res[2][1] == "peer self-check failed on another rank"
 
 
+def _peer_fail_worker(rank, world, port, q):
+    """Host side of the fused peer combine's failure path, one gloo rank each.
+    The device launch is simulated: call 1 succeeds everywhere; in call 2 rank 1
+    never publishes, so rank 0's kernel stamps (epoch 2, missing {1}) and yields
+    NaN while rank 1 completes (its peers did publish); in call 3 rank 0 has
+    retired the peer path, so rank 1's kernel stamps (epoch 3, missing {0})."""
+    sys.path.insert(0, REPO)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1401_0248_b200 import dist as D
+    import paper_1401_0248_b200 as tfb
+    pc = D._PeerCombine.__new__(D._PeerCombine)
+    pc.world, pc.rank, pc.epoch, pc.failed = world, rank, 0, None
+    pc.error = torch.zeros(2, dtype=torch.int32)
+
+    def launch(pc_, epoch):
+        if (epoch == 2 and rank == 0) or (epoch == 3 and rank == 1):
+            pc_.error[1] = 1 << (1 - rank)
+            pc_.error[0] = epoch
+            return torch.full((2,), float("nan"), dtype=torch.float64)
+        return torch.tensor([1.0 + rank, 0.0], dtype=torch.float64)
+
+    x = torch.zeros(8, dtype=torch.float64)
+    log = []
+    for call in (1, 2, 3, 4):
+        try:
+            out = D._reduce_peer(tfb.Method.TWOFOLD_FAST, x, None, 10, None, False, pc=pc, launch=launch)
+            log.append(("ok", float(out[0])))
+        except D.PeerTimeout as exc:
+            log.append(("timeout", str(exc)))
+    # the NCCL/gloo combine still works for every rank after the peer path is retired
+    pair = D.sharded_reduce(tfb.Method.TWOFOLD_FAST, torch.tensor([float(rank)]), None, n_global=2,
+                            local_reduce=lambda m, xl, yl, lg: torch.tensor([float(xl[0]), 0.0], dtype=torch.float64),
+                            merge=lambda m, pairs: pairs.sum(0))
+    q.put((rank, log, pair.tolist(), pc.failed))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_peer_timeout_raises_instead_of_nan():
+    """a peer timeout must raise on the host (never hand back NaN), is
+    stamped per call (not sticky: the stale stamp of call 2 does not fail call 1's
+    successor on the other rank), and retires the peer path on the failing rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_fail_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r: (log, pair, failed) for r, log, pair, failed in (q.get(timeout=300) for _ in range(2))}
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    log0, pair0, failed0 = res[0]
+    log1, pair1, failed1 = res[1]
+    assert log0[0] == ("ok", 1.0) and log0[1][0] == "timeout" and "rank(s) [1]" in log0[1][1]
+    assert log0[2][0] == log0[3][0] == "timeout" and "retired" in log0[2][1]  # no silent NaN afterwards
+    assert log1[0] == ("ok", 2.0) and log1[1] == ("ok", 2.0)  # call 2 completed on the late rank
+    assert log1[2][0] == "timeout" and "rank(s) [0]" in log1[2][1] and log1[3][0] == "timeout"
+    assert failed0 and failed1
+    assert pair0 == pair1 == [1.0, 0.0]
+
+
 def test_ragged_shards_cover_everything(oracle):
     """Non-power-of-two n: shards are leaf-aligned and the merged pair still tracks the exact sum."""
     n = 300_007

@@ -39,7 +39,8 @@ def _report():
 def tfb(cuda):
     import paper_1401_0248_b200 as m
     torch.cuda.set_device(cuda)
-    yield m
+    with m.using_flavor("cuda"):  # the wrappers on the grid flavor for this module
+        yield m
     _report()
 
 

@@ -16,7 +16,8 @@ pytestmark = pytest.mark.gpu
 def tfb(cuda):
     import paper_1401_0248_b200 as m
     torch.cuda.set_device(cuda)
-    return m
+    with m.using_flavor("cuda"):  # the wrappers on the grid flavor for this module
+        yield m
 
 
 def test_fuzz_grid_vs_emulator(tfb, oracle, cuda):

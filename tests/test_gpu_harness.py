@@ -29,11 +29,37 @@ def test_hours100_seq_goldens_and_grid(H):
     assert grid["twofold-fast"].deviation_hours <= 1.5e-6 and grid["kahan"].deviation_hours < 1e-5
 
 
+def test_accuracy_bands_default_wrappers_c4(H, cuda):
+    """C4 exactly as the reference states it (test_acceptance.py:133-164), through the
+    package's DEFAULT wrappers (the seq flavor): f32 bands 1e-8 <= direct <= 1e-3,
+    kahan <= 1e-7, twofold <= 1e-9; f64 twofold-fast v+e within 1e-30 of the exact
+    sum, judged in rationals; and under 30 s."""
+    import time
+    import paper_1401_0248_b200 as tfb
+    t0 = time.perf_counter()
+    for gen in tfb.LcgKind:
+        for sym in (False, True):
+            x = tfb.fill(gen, 1_000_000, 1, np.float32, sym=sym)
+            ref = tfb.exact_sum(x)
+            rel_d = abs(tfb.relative_error(float(np.float64(tfb.sum_direct(x).value)), ref))
+            kah = tfb.run_flavor(tfb.Method.KAHAN, tfb.Flavor.sequential(), x)
+            rel_k = abs(tfb.relative_error(float(np.float64(kah.value)), ref))
+            tf = tfb.sum_twofold_fast(x)
+            rel_t = abs(tfb.relative_error(float(np.float64(tf.value)) + float(np.float64(tf.error)), ref))
+            assert 1e-8 <= rel_d <= 1e-3 and rel_k <= 1e-7 and rel_t <= 1e-9, (gen, sym, rel_d, rel_k, rel_t)
+        x = tfb.fill(gen, 1_000_000, 1, np.float64)
+        ref_q = sum((Fraction(c) for c in tfb.exact_sum(x).components), Fraction(0))
+        tf = tfb.sum_twofold_fast(x)
+        assert abs((Fraction(float(tf.value)) + Fraction(float(tf.error)) - ref_q) / ref_q) <= Fraction(1, 10 ** 30)
+    assert time.perf_counter() - t0 < 30.0
+
+
 def test_accuracy_bands_grid_flavor(H):
     """C4 (test_acceptance.py:133-164) upper bands on the grid flavor (a tree sum is
     more accurate than sequential, so the direct lower band does not apply)."""
     import paper_1401_0248_b200 as tfb
-    rows = H.run_accuracy_table(n=1_000_000)
+    cuda_fl = tfb.Flavor.cuda()
+    rows = H.run_accuracy_table(n=1_000_000, flavor=cuda_fl)
     for r in rows:
         if r.precision == "f32":
             limit = {"direct": 1e-3, "kahan": 1e-7, "twofold-fast": 1e-9}[r.method]
@@ -48,9 +74,9 @@ def test_accuracy_bands_grid_flavor(H):
         x = tfb.lcg_fill(gen, 1_000_000, 1, torch.float64)
         ref = tfb.exact_sum(x).fraction()
         A = tfb.exact_sum(x, absolute=True).fraction()
-        r = tfb.sum_twofold_rigorous(x)
+        r = tfb.sum_twofold_rigorous(x, flavor=cuda_fl)
         assert abs((Fraction(float(r.value)) + Fraction(float(r.error)) - ref) / ref) <= Fraction(1, 10 ** 30)
-        f = tfb.sum_twofold_fast(x)
+        f = tfb.sum_twofold_fast(x, flavor=cuda_fl)
         D = abs(Fraction(float(f.value)) + Fraction(float(f.error)) - ref)
         assert D <= 2 * 10 ** 6 * eps * eps * A + eps * A / 64
         s = tfb.run_flavor(tfb.Method.TWOFOLD_FAST, tfb.Flavor.sequential(), x)
@@ -59,7 +85,8 @@ def test_accuracy_bands_grid_flavor(H):
 
 def test_scaling_twofold_beats_direct(H):
     """C5 spirit (test_acceptance.py:167-177): twofold >= 10x better than direct at every n >= 1e4."""
-    pts, slopes = H.run_scaling_study(ns=(10 ** 4, 10 ** 5, 10 ** 6), trials=10)
+    import paper_1401_0248_b200 as tfb
+    pts, slopes = H.run_scaling_study(ns=(10 ** 4, 10 ** 5, 10 ** 6), trials=10, flavor=tfb.Flavor.cuda())
     by = {(n, m): e for n, m, e in pts}
     for n in (10 ** 4, 10 ** 5, 10 ** 6):
         assert by[(n, "twofold-fast")] <= by[(n, "direct")] / 10
@@ -90,7 +117,7 @@ def test_error_sign_fidelity_grid(H):
         for sym in (False, True):
             data = tfb.lcg_fill("mmix", 1_000_000, seed, torch.float32, sym)
             ref = tfb.exact_sum(data)
-            r = tfb.sum_twofold_fast(data)
+            r = tfb.sum_twofold_fast(data, flavor="cuda")
             rel_value = tfb.relative_error(float(np.float64(r.value)), ref)
             if abs(rel_value) > 10 * 2.0 ** -24:
                 assert math.copysign(1, float(r.error)) == math.copysign(1, float(ref) - float(r.value))
@@ -99,7 +126,7 @@ def test_error_sign_fidelity_grid(H):
     # also check the sign on cancellation-heavy cfg3-style data where it always does
     x = tfb.philox_fill("illcond", 1 << 22, seed=2, total=1 << 22)
     ref = tfb.exact_sum(x)
-    r = tfb.sum_twofold_rigorous(x)
+    r = tfb.sum_twofold_rigorous(x, flavor="cuda")
     assert math.copysign(1, float(r.error)) == math.copysign(1, float(ref.hi) - float(r.value))
 
 

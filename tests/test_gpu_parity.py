@@ -23,9 +23,12 @@ SIZES = [0, 1, 2, 3, 5, 17, 255, 256, 1023, 1024, 1025, 4095, 4096, 4097, 8191, 
 
 @pytest.fixture(scope="module")
 def tfb(cuda):
+    """The package with the wrappers switched to the grid flavor for this module
+    (their default is the reference's seq bits; tests/test_gpu_dropin.py covers that)."""
     import paper_1401_0248_b200 as m
     torch.cuda.set_device(cuda)
-    return m
+    with m.using_flavor("cuda"):
+        yield m
 
 
 def _methods(dt):
