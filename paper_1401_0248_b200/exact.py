@@ -156,7 +156,10 @@ def _exact(x: torch.Tensor, y: torch.Tensor | None, flags: int) -> ExactValue:
                              flags, out.data_ptr(), limbs.data_ptr(), buf.data_ptr(), nbytes.value,
                              counter.data_ptr(), _stream_ptr(dev)), "tf_exact")
     hi, lo = out.cpu().tolist()
-    ev = ExactValue.from_limbs(tuple(limbs.cpu().tolist()))
+    lt = tuple(limbs.cpu().tolist())
+    if not math.isfinite(hi):  # a non-finite addend: the device reports inf / nan, the limbs hold the finite part
+        return ExactValue((lo, hi) if lo != 0 else (hi,), lt)
+    ev = ExactValue.from_limbs(lt)
     if math.isfinite(ev.hi) and (ev.hi, ev.lo) != (hi, lo):  # the device's own rounding of the limbs must agree
         raise RuntimeError(f"tf_exact: leading components ({hi!r}, {lo!r}) disagree with the limbs {ev.components!r}")
     return ev

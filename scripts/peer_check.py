@@ -58,7 +58,7 @@ def main():
         used = tfb.combine_in_use(None, dev, acc)
         assert used == "peer", used
     if world > 1:  # auto then routes device shards through the fused kernel
-        got = tfb.sharded_reduce(tfb.Method.TWOFOLD_FAST, x, y, n_global=n_global).cpu()
+        got = tfb.sharded_reduce(tfb.Method.TWOFOLD_FAST, x, y, n_global=n_global, combine="auto").cpu()
         ref = tfb.sharded_reduce(tfb.Method.TWOFOLD_FAST, x, y, n_global=n_global, combine="nccl").cpu()
         assert torch.equal(got, ref)
     dist.barrier()

@@ -69,7 +69,7 @@ def test_exact_sum_and_dot_match_reference(twofold, dropin):
         # hi/lo of two equal expansions can differ by representation, so compare to 2^-40
         got = twofold.relative_error(float(twofold.sum_direct(x).value), es)
         want = float.fromhex(rec["rel_sum_direct"])
-        assert abs(got - want) <= 2.0 ** -40 * abs(want) + 1e-300, (rec, got, want)
+        assert abs(got - want) <= 2.0 ** -60 + 2.0 ** -40 * abs(want), (rec, got, want)
 
 
 def test_default_wrappers_return_reference_seq_bits(twofold, golden, oracle):
@@ -99,7 +99,10 @@ def test_default_wrappers_return_reference_seq_bits(twofold, golden, oracle):
 def test_accuracy_harness_reproduces_reference(twofold, dropin):
     """accuracy.run_accuracy_table(n=100000) and run_scaling_study on the GPU seq path
     (the reference's flavor) give the reference's numbers: identical method results,
-    relative errors equal up to the leading-component representation (2^-40)."""
+    relative errors equal up to the leading-component representation.  The
+    reference's expansion is non-overlapping but not canonical, so its hi + lo can
+    miss S by a third component as large as lo/2 (~2^-54 S); ours is the
+    nearest-rounding decomposition.  Hence |delta| <= 2^-60 + 2^-40 |rel|."""
     from paper_1401_0248_b200 import harness
     want = {(r["precision"], r["generator"], r["interval"], r["method"]): r for r in dropin["accuracy_table"]["rows"]}
     rows = harness.run_accuracy_table(n=100_000, seed=1)
@@ -107,12 +110,12 @@ def test_accuracy_harness_reproduces_reference(twofold, dropin):
     for r in rows:
         w = want[(r.precision, r.generator, r.interval, r.method)]
         wv = float.fromhex(w["rel_error"])
-        assert r.valid == w["valid"] and abs(r.rel_error - wv) <= 2.0 ** -40 * abs(wv), (r, wv)
+        assert r.valid == w["valid"] and abs(r.rel_error - wv) <= 2.0 ** -60 + 2.0 ** -40 * abs(wv), (r, wv)
     st = dropin["scaling_study"]
     pts, slopes = harness.run_scaling_study(ns=tuple(st["ns"]), trials=st["trials"], seed=st["seed"])
     wm = {(r["n"], r["method"]): float.fromhex(r["median"]) for r in st["rows"]}
     for n, m, med in pts:
-        assert abs(med - wm[(n, m)]) <= 2.0 ** -40 * wm[(n, m)], (n, m, med, wm[(n, m)])
+        assert abs(med - wm[(n, m)]) <= 2.0 ** -60 + 2.0 ** -40 * wm[(n, m)], (n, m, med, wm[(n, m)])
     for m, s in st["slopes"].items():
         assert (slopes[m] is None) == (s is None)
         if s is not None:

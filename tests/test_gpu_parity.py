@@ -526,7 +526,8 @@ def test_gpu_exact_sum_matches_expansion_oracle(tfb, oracle, golden, cuda):
     for name, rec in golden["inputs"].items():
         x, y = inputs[name]
         ref = sum((Fraction(float.fromhex(c)) for c in rec["exact"]), Fraction(0))
-        got = tfb.exact_sum(x) if y is None else tfb.exact_dot(x, y)
+        # the fixture's dot oracle is over the kernels' addends (products rounded in the data type)
+        got = tfb.exact_sum(x) if y is None else tfb.exact_dot(x, y, rounded_products=True)
         assert got.fraction() == ref, name
         assert got.hi == float(ref) if ref else got.hi == 0.0
         if ref:
@@ -553,11 +554,14 @@ def test_gpu_exact_hard_cases(tfb, oracle, cuda):
                                 else oracle.abs_sum(x))
     xf = oracle.lcg_fill("mmix", 300_001, 4, np.float32, True)
     yf = oracle.lcg_fill("nr", 300_001, 5, np.float32, True)
-    assert tfb.exact_dot(xf, yf).fraction() == oracle.exact(xf, yf)
+    assert tfb.exact_dot(xf, yf, rounded_products=True).fraction() == oracle.exact(xf, yf)
     assert tfb.exact_dot(xf, yf, true_products=True).fraction() == oracle.exact_true_dot(xf, yf)
+    # default = expansion.exact_dot (expansion.py:112-126): binary32 sums the exact products
+    assert tfb.exact_dot(xf, yf).fraction() == oracle.exact_true_dot(xf, yf)
     xd = oracle.lcg_fill("mmix", 300_001, 4, np.float64, True)
     yd = oracle.lcg_fill("nr", 300_001, 5, np.float64, True)
     assert tfb.exact_dot(xd, yd, true_products=True).fraction() == oracle.exact_true_dot(xd, yd)
+    assert tfb.exact_dot(xd, yd).fraction() == oracle.exact(xd, yd)  # binary64: rounded products
     assert np.isnan(tfb.exact_sum(np.array([1.0, np.inf])).hi)
     # grid independence: a slice reduced in place == its copy
     xt = torch.from_numpy(xd).to(cuda)
