@@ -585,7 +585,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     n0 = _tl.lib().tf_launch_count()
-    with clocks:
+    with clocks, torch.cuda.nvtx.range("bench: timed steps"):
         elapsed_ms = timed(step)
     # kernels this library launched for the timed steps (graph mode: counted at capture,
     # i.e. the launches of the one timed replay)
@@ -672,9 +672,10 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
         w0 = time.perf_counter()
-        for _ in range(ke):
-            e2e_step()
-        torch.cuda.synchronize()
+        with torch.cuda.nvtx.range("bench: e2e steps"):
+            for _ in range(ke):
+                e2e_step()
+            torch.cuda.synchronize()
         wall = time.perf_counter() - w0
         if use_dist:
             tw = torch.tensor([wall], dtype=torch.float64, device=dev)

@@ -36,10 +36,18 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: ranges cost nothing unless a tool is attached
+
 #include "status.h"
 
 namespace tfb {
 namespace {
+
+// NVTX range for the host-side stages (ncu --nvtx / Nsight timelines).
+struct Range {
+  explicit Range(const char* name) { nvtxRangePushA(name); }
+  ~Range() { nvtxRangePop(); }
+};
 
 // Fixed-size pool: copy(dst, src, bytes) splits the range into one piece per
 // worker (plus the calling thread) and returns when all pieces are done.
@@ -276,6 +284,87 @@ int stage(HostEngine* g, cudaStream_t s, int b, int k, const char* src, size_t b
   return TF_OK;
 }
 
+
+size_t pair_size(int method, int dtype) {
+  const int base = method & ~TF_TRACK_PRODUCT;
+  return (base == TF_WIDE ? 8 : (dtype == TF_F64 ? 8 : 4)) * 2;
+}
+
+// Order the engine's streams after the caller's stream when an operand is device
+// or page-locked memory the caller may still be writing.
+int after_caller(HostEngine* g, Mem kx, Mem ky, void* after_stream) {
+  if (kx == Mem::kPageable && ky == Mem::kPageable) return TF_OK;
+  int rc;
+  if ((rc = cu(cudaEventRecord(g->entry, static_cast<cudaStream_t>(after_stream))))) return rc;
+  if ((rc = cu(cudaStreamWaitEvent(g->stream, g->entry, 0)))) return rc;
+  return cu(cudaStreamWaitEvent(g->cstream, g->entry, 0));
+}
+
+// The staged path for host operands (pageable or page-locked) of n elements at
+// leaf size lg: up to one chunk -> stage + tf_reduce; more -> leaf-aligned
+// chunks, the DMA of chunk c+1 (copy stream) overlapping the leaves of chunk c
+// (compute stream), then tf_merge_tree.  Chunks are whole leaves, so the result
+// is bit-identical to tf_reduce on the whole array.  The pair lands in `out`
+// (mapped pinned memory); returns after the streams drained.
+int staged_reduce(HostEngine* g, int method, int dtype, const char* cx, const char* cy, int64_t n, int lg,
+                  Mem kx, Mem ky, void* out) {
+  Range range("staged_reduce");
+  const size_t pair_bytes = pair_size(method, dtype);
+  const size_t item = dtype == TF_F64 ? 8 : 4;
+  const bool dot = cy != nullptr;
+  size_t pb = 0;
+  int64_t cnt = 0, leaves = 0;
+  int rc = tf_workspace_size(method, dtype, 1, n, lg, &pb, &cnt, &leaves);
+  if (rc) return rc;
+  if ((rc = ensure_scratch(g, std::max<size_t>(pb, pair_bytes), std::max<int64_t>(cnt, 1)))) return rc;
+  const int64_t L = int64_t(1) << lg;
+  // slot size: the whole input up to the target, never less than one leaf
+  const size_t want = std::max(std::min(static_cast<size_t>(n) * item, g->chunk_target),
+                               static_cast<size_t>(std::min<int64_t>(L, n)) * item);
+  if ((rc = grow_slots(g, want))) return rc;
+  const int64_t chunk_leaves = std::max<int64_t>(1, static_cast<int64_t>(g->chunk / (L * item)));
+  const int64_t chunk_elems = chunk_leaves * L;
+  if (n <= chunk_elems) {
+    const size_t bytes = n * item;
+    if (n > 0) {
+      Range r("h2d");
+      if ((rc = stage(g, g->stream, 0, 0, cx, bytes, kx, true))) return rc;
+      if (dot && (rc = stage(g, g->stream, 0, 1, cy, bytes, ky, true))) return rc;
+      if ((rc = cu(cudaEventRecord(g->h2d_done[0], g->stream)))) return rc;
+    }
+    rc = tf_reduce(method, dtype, g->dev[0], dot ? g->dev[0] + g->chunk : nullptr, n, lg, out, g->partials,
+                   g->partials_bytes, g->counters, g->counters_len, g->stream);
+  } else {
+    const int64_t nchunks = (n + chunk_elems - 1) / chunk_elems;
+    for (int64_t c = 0; c < nchunks && rc == TF_OK; ++c) {
+      Range r("chunk");
+      const int b = static_cast<int>(c & 1);
+      const int64_t lo = c * chunk_elems;
+      const int64_t m = std::min(n, lo + chunk_elems) - lo;
+      const size_t bytes = m * item;
+      // Copies on cstream, leaf kernels on stream: the DMA of chunk c+1 overlaps
+      // the leaves of chunk c.  Slot b is reused by chunk c+2 only after
+      // kernel c finished (device side) and DMA c drained (host side, pageable).
+      if (c >= 2 && (rc = cu(cudaStreamWaitEvent(g->cstream, g->k_done[b], 0)))) break;
+      if ((rc = stage(g, g->cstream, b, 0, cx + lo * item, bytes, kx, c >= 2))) break;
+      if (dot && (rc = stage(g, g->cstream, b, 1, cy + lo * item, bytes, ky, c >= 2))) break;
+      if ((rc = cu(cudaEventRecord(g->h2d_done[b], g->cstream)))) break;
+      if ((rc = cu(cudaStreamWaitEvent(g->stream, g->h2d_done[b], 0)))) break;
+      rc = tf_reduce_leaves(method, dtype, g->dev[b], dot ? g->dev[b] + g->chunk : nullptr, m, lg,
+                            static_cast<char*>(g->partials) + c * chunk_leaves * pair_bytes, g->stream);
+      if (rc == TF_OK) rc = cu(cudaEventRecord(g->k_done[b], g->stream));
+    }
+    if (rc == TF_OK) rc = tf_merge_tree(method, dtype, g->partials, leaves, out, g->stream);
+  }
+  if (rc) {
+    cudaStreamSynchronize(g->cstream);
+    cudaStreamSynchronize(g->stream);
+    return rc;
+  }
+  rc = cu(cudaStreamSynchronize(g->stream));
+  if (rc == TF_OK) rc = cu(cudaStreamSynchronize(g->cstream));
+  return rc;
+}
 }  // namespace
 }  // namespace tfb
 
@@ -353,8 +442,8 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
   auto* g = static_cast<HostEngine*>(engine);
   std::lock_guard<std::mutex> lk(g->mu);
   tfb::DeviceGuard guard(g->device);
-  const int base = method & ~TF_TRACK_PRODUCT;
-  const size_t pair_bytes = (base == TF_WIDE ? 8 : (dtype == TF_F64 ? 8 : 4)) * 2;
+  tfb::Range range("tf_host_reduce");
+  const size_t pair_bytes = tfb::pair_size(method, dtype);
   const size_t item = dtype == TF_F64 ? 8 : 4;
   const bool dot = hy != nullptr;
 
@@ -370,100 +459,58 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
   if (kx == tfb::Mem::kOtherDevice || ky == tfb::Mem::kOtherDevice) return TF_EINVAL_ARG;
   // Device or page-locked operands may still be in flight on the caller's
   // stream (NULL = the legacy default stream): order the engine's streams after it.
-  if (kx != tfb::Mem::kPageable || ky != tfb::Mem::kPageable) {
-    if ((rc = tfb::cu(cudaEventRecord(g->entry, static_cast<cudaStream_t>(after_stream))))) return rc;
-    if ((rc = tfb::cu(cudaStreamWaitEvent(g->stream, g->entry, 0)))) return rc;
-    if ((rc = tfb::cu(cudaStreamWaitEvent(g->cstream, g->entry, 0)))) return rc;
-  }
+  if ((rc = tfb::after_caller(g, kx, ky, after_stream))) return rc;
   if (kx == tfb::Mem::kDevice && ky == tfb::Mem::kDevice) {  // already resident: plain tf_reduce
     rc = tf_reduce(method, dtype, hx, hy, n, leaf_log2, g->pair_pin, g->partials, g->partials_bytes,
                    g->counters, g->counters_len, g->stream);
-  } else if (kx == tfb::Mem::kDevice || ky == tfb::Mem::kDevice) {
-    return TF_EINVAL_ARG;  // mixed host/device operands
-  } else {
-    const int64_t L = int64_t(1) << lg;
-    // slot size for this call: the whole input up to the target, never less than one leaf
-    const size_t want = std::max(std::min(static_cast<size_t>(n) * item, g->chunk_target),
-                                 static_cast<size_t>(std::min<int64_t>(L, n)) * item);
-    if ((rc = tfb::grow_slots(g, want))) return rc;
-    const int64_t chunk_leaves = std::max<int64_t>(1, static_cast<int64_t>(g->chunk / (L * item)));
-    const int64_t chunk_elems = chunk_leaves * L;
-    const auto* cx = static_cast<const char*>(hx);
-    const auto* cy = static_cast<const char*>(hy);
-    const size_t bytes_all = static_cast<size_t>(n) * item;
-    const bool pageable = kx == tfb::Mem::kPageable || (dot && ky == tfb::Mem::kPageable);
-    if (n > 0 && bytes_all <= (pageable ? tfb::kZeroCopyMaxPageable : tfb::kZeroCopyMaxPinned)) {
-      // Small input: no DMA at all.  The kernel reads the operands over PCIe
-      // straight from page-locked host memory (the staging slot, or the caller's
-      // own pinned buffer); one launch, one sync.
-      const void* dx = hx;
-      const void* dy = hy;
-      if (kx == tfb::Mem::kPageable) {
-        std::memcpy(g->pin[0], cx, bytes_all);
-        dx = g->pin[0];
-      } else if (cudaHostGetDevicePointer(const_cast<void**>(&dx), const_cast<void*>(hx), 0) != cudaSuccess) {
+    if (rc == TF_OK) rc = tfb::cu(cudaStreamSynchronize(g->stream));
+    if (rc) {
+      cudaStreamSynchronize(g->stream);
+      return rc;
+    }
+    std::memcpy(out_pair_host, g->pair_pin, pair_bytes);
+    return TF_OK;
+  }
+  if (kx == tfb::Mem::kDevice || ky == tfb::Mem::kDevice) return TF_EINVAL_ARG;  // mixed host/device operands
+  const auto* cx = static_cast<const char*>(hx);
+  const auto* cy = static_cast<const char*>(hy);
+  const size_t bytes_all = static_cast<size_t>(n) * item;
+  const bool pageable = kx == tfb::Mem::kPageable || (dot && ky == tfb::Mem::kPageable);
+  if (n > 0 && bytes_all <= (pageable ? tfb::kZeroCopyMaxPageable : tfb::kZeroCopyMaxPinned)) {
+    // Small input: no DMA at all.  The kernel reads the operands over PCIe
+    // straight from page-locked host memory (the staging slot, or the caller's
+    // own pinned buffer); one launch, one sync.
+    const void* dx = hx;
+    const void* dy = hy;
+    if (kx == tfb::Mem::kPageable) {
+      std::memcpy(g->pin[0], cx, bytes_all);
+      dx = g->pin[0];
+    } else if (cudaHostGetDevicePointer(const_cast<void**>(&dx), const_cast<void*>(hx), 0) != cudaSuccess) {
+      cudaGetLastError();
+      dx = nullptr;
+    }
+    if (dot) {
+      if (ky == tfb::Mem::kPageable) {
+        std::memcpy(g->pin[0] + g->chunk, cy, bytes_all);
+        dy = g->pin[0] + g->chunk;
+      } else if (cudaHostGetDevicePointer(const_cast<void**>(&dy), const_cast<void*>(hy), 0) != cudaSuccess) {
         cudaGetLastError();
-        dx = nullptr;
-      }
-      if (dot) {
-        if (ky == tfb::Mem::kPageable) {
-          std::memcpy(g->pin[0] + g->chunk, cy, bytes_all);
-          dy = g->pin[0] + g->chunk;
-        } else if (cudaHostGetDevicePointer(const_cast<void**>(&dy), const_cast<void*>(hy), 0) != cudaSuccess) {
-          cudaGetLastError();
-          dy = nullptr;
-        }
-      }
-      if (dx && (!dot || dy)) {
-        rc = tf_reduce(method, dtype, dx, dot ? dy : nullptr, n, lg, g->pair_pin, g->partials, g->partials_bytes,
-                       g->counters, g->counters_len, g->stream);
-        if (rc) {
-          cudaStreamSynchronize(g->stream);
-          return rc;
-        }
-        if ((rc = tfb::cu(cudaStreamSynchronize(g->stream)))) return rc;
-        std::memcpy(out_pair_host, g->pair_pin, pair_bytes);
-        return TF_OK;
+        dy = nullptr;
       }
     }
-    if (n <= chunk_elems) {
-      const size_t bytes = n * item;
-      if (n > 0) {
-        if ((rc = tfb::stage(g, g->stream, 0, 0, cx, bytes, kx, true))) return rc;
-        if (dot && (rc = tfb::stage(g, g->stream, 0, 1, cy, bytes, ky, true))) return rc;
-        if ((rc = tfb::cu(cudaEventRecord(g->h2d_done[0], g->stream)))) return rc;
+    if (dx && (!dot || dy)) {
+      rc = tf_reduce(method, dtype, dx, dot ? dy : nullptr, n, lg, g->pair_pin, g->partials, g->partials_bytes,
+                     g->counters, g->counters_len, g->stream);
+      if (rc) {
+        cudaStreamSynchronize(g->stream);
+        return rc;
       }
-      rc = tf_reduce(method, dtype, g->dev[0], dot ? g->dev[0] + g->chunk : nullptr, n, lg, g->pair_pin,
-                     g->partials, g->partials_bytes, g->counters, g->counters_len, g->stream);
-    } else {
-      const int64_t nchunks = (n + chunk_elems - 1) / chunk_elems;
-      for (int64_t c = 0; c < nchunks && rc == TF_OK; ++c) {
-        const int b = static_cast<int>(c & 1);
-        const int64_t lo = c * chunk_elems;
-        const int64_t m = std::min(n, lo + chunk_elems) - lo;
-        const size_t bytes = m * item;
-        // Copies on cstream, leaf kernels on stream: the DMA of chunk c+1 overlaps
-        // the leaves of chunk c.  Slot b is reused by chunk c+2 only after
-        // kernel c finished (device side) and DMA c drained (host side, pageable).
-        if (c >= 2 && (rc = tfb::cu(cudaStreamWaitEvent(g->cstream, g->k_done[b], 0)))) break;
-        if ((rc = tfb::stage(g, g->cstream, b, 0, cx + lo * item, bytes, kx, c >= 2))) break;
-        if (dot && (rc = tfb::stage(g, g->cstream, b, 1, cy + lo * item, bytes, ky, c >= 2))) break;
-        if ((rc = tfb::cu(cudaEventRecord(g->h2d_done[b], g->cstream)))) break;
-        if ((rc = tfb::cu(cudaStreamWaitEvent(g->stream, g->h2d_done[b], 0)))) break;
-        rc = tf_reduce_leaves(method, dtype, g->dev[b], dot ? g->dev[b] + g->chunk : nullptr, m, lg,
-                              static_cast<char*>(g->partials) + c * chunk_leaves * pair_bytes, g->stream);
-        if (rc == TF_OK) rc = tfb::cu(cudaEventRecord(g->k_done[b], g->stream));
-      }
-      if (rc == TF_OK)
-        rc = tf_merge_tree(method, dtype, g->partials, leaves, g->pair_pin, g->stream);
+      if ((rc = tfb::cu(cudaStreamSynchronize(g->stream)))) return rc;
+      std::memcpy(out_pair_host, g->pair_pin, pair_bytes);
+      return TF_OK;
     }
   }
-  if (rc) {
-    cudaStreamSynchronize(g->cstream);
-    cudaStreamSynchronize(g->stream);
-    return rc;
-  }
-  if ((rc = tfb::cu(cudaStreamSynchronize(g->stream)))) return rc;
+  if ((rc = tfb::staged_reduce(g, method, dtype, cx, cy, n, lg, kx, ky, g->pair_pin))) return rc;
   std::memcpy(out_pair_host, g->pair_pin, pair_bytes);
   return TF_OK;
 }
@@ -482,8 +529,8 @@ int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, con
   auto* g = static_cast<HostEngine*>(engine);
   std::lock_guard<std::mutex> lk(g->mu);
   tfb::DeviceGuard guard(g->device);
-  const int base = method & ~TF_TRACK_PRODUCT;
-  const size_t pair_bytes = (base == TF_WIDE ? 8 : (dtype == TF_F64 ? 8 : 4)) * 2;
+  tfb::Range range("tf_host_reduce_rows");
+  const size_t pair_bytes = tfb::pair_size(method, dtype);
   const size_t item = dtype == TF_F64 ? 8 : 4;
   const bool dot = hy != nullptr;
   // the leaf size is the WHOLE matrix's (tf_reduce_rows resolves it from rows * cols),
@@ -506,20 +553,26 @@ int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, con
   const tfb::Mem kx = cols > 0 ? tfb::classify(hx, g->device) : tfb::Mem::kPageable;
   const tfb::Mem ky = dot && cols > 0 ? tfb::classify(hy, g->device) : kx;
   if (kx == tfb::Mem::kOtherDevice || ky == tfb::Mem::kOtherDevice) return TF_EINVAL_ARG;
-  if (kx != tfb::Mem::kPageable || ky != tfb::Mem::kPageable) {
-    if ((rc = tfb::cu(cudaEventRecord(g->entry, static_cast<cudaStream_t>(after_stream))))) return rc;
-    if ((rc = tfb::cu(cudaStreamWaitEvent(g->stream, g->entry, 0)))) return rc;
-    if ((rc = tfb::cu(cudaStreamWaitEvent(g->cstream, g->entry, 0)))) return rc;
-  }
+  if ((rc = tfb::after_caller(g, kx, ky, after_stream))) return rc;
+  const size_t row_bytes = static_cast<size_t>(cols) * item;
   if (kx == tfb::Mem::kDevice && ky == tfb::Mem::kDevice) {
     rc = tf_reduce_rows(method, dtype, hx, hy, rows, cols, ldx, ldy, lg, g->rows_pin, g->partials,
                         g->partials_bytes, g->counters, g->counters_len, g->stream);
   } else if (kx == tfb::Mem::kDevice || ky == tfb::Mem::kDevice) {
     return TF_EINVAL_ARG;  // mixed host/device operands
+  } else if (row_bytes > g->chunk_target) {
+    // Rows longer than a staging slot stream through leaf-aligned chunks, one row
+    // at a time (the 1-D staged path at the matrix's leaf size, so each row is
+    // bit-identical to tf_reduce_rows), instead of sizing the slots to a whole row.
+    const auto* cx = static_cast<const char*>(hx);
+    const auto* cy = static_cast<const char*>(hy);
+    for (int64_t r = 0; r < rows && rc == TF_OK; ++r)
+      rc = tfb::staged_reduce(g, method, dtype, cx + static_cast<size_t>(r) * ldx * item,
+                              dot ? cy + static_cast<size_t>(r) * ldy * item : nullptr, cols, lg, kx, ky,
+                              static_cast<char*>(g->rows_pin) + static_cast<size_t>(r) * pair_bytes);
   } else {
     // Row blocks, packed (leading dimension = cols) into the staging slots; the
     // copies of block b+1 (copy stream) overlap the reduction of block b.
-    const size_t row_bytes = static_cast<size_t>(cols) * item;
     const size_t want = std::min(static_cast<size_t>(rows) * row_bytes, g->chunk_target);
     if ((rc = tfb::grow_slots(g, std::max(want, row_bytes)))) return rc;
     const int64_t block = std::max<int64_t>(1, static_cast<int64_t>(g->chunk / std::max<size_t>(row_bytes, 1)));

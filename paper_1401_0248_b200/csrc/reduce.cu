@@ -836,7 +836,10 @@ static int launch_small(const T* px, const T* py, int64_t n, int64_t P, void* ou
 // CTA per row above (LDG 6.3-6.5 TB/s
 // from 16 to 128 KiB rows; the TMA pipeline from 256 KiB rows, cfg4).
 constexpr int64_t kShortRowMaxBytes = int64_t(16) << 10;
-constexpr int64_t kShortRowMaxScalarCols = 700;  // misaligned binary64 (513 columns: 3.45 vs 2.87 TB/s, 777: 3.35 vs 3.74)
+// misaligned pitches: lane groups up to 1024 columns, a CTA per row (shifted-vector /
+// batched element loads) above (profiles/r02_rows_misaligned.txt: f32 1001 columns 3.5 vs
+// 3.4 TB/s, 4099: 3.3 vs 6.0; f64 1001: 4.6 vs 4.5, 4099: 4.7 vs 5.7)
+constexpr int64_t kShortRowMaxMisCols = 1024;
 constexpr int64_t kTmaRowMinBytes = int64_t(256) << 10;
 static int g_rows_kernel = -1;
 static int rows_kernel_choice() {
@@ -945,10 +948,9 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
   // Many rows of at most one leaf each: a group of lanes per row (rows.cuh).
   if (fused && !peer && rows > 1 && P == 1) {
     const int rk = rows_kernel_choice();
-    // misaligned pitches: lane blocks use aligned loads + selects; binary32 up to 16 KiB
-    // rows, binary64 below 700 columns (a CTA per row wins above)
-    if (rk == 2 || (rk == 0 && ((vec || sizeof(T) == 4) ? cols * int64_t(sizeof(T)) <= kShortRowMaxBytes
-                                                        : cols < kShortRowMaxScalarCols))) {
+    // aligned rows up to 16 KiB per operand, misaligned pitches up to 1024 columns (lane
+    // blocks with aligned loads + selects); a CTA per row above
+    if (rk == 2 || (rk == 0 && (vec ? cols * int64_t(sizeof(T)) <= kShortRowMaxBytes : cols <= kShortRowMaxMisCols))) {
       auto a32 = [](const void* p, int64_t ld) {
         return (reinterpret_cast<uintptr_t>(p) & 31u) == 0 && (ld * int64_t(sizeof(T))) % 32 == 0;
       };

@@ -50,6 +50,44 @@ __device__ __forceinline__ void ld_stream32(const double2* p, double2& a, double
       : "l"(p));
 }
 
+// Misaligned lane blocks: 16-byte __ldg vectors (binary32) or 32-byte windows
+// (binary64); measured per dtype (profiles/r02_rows_misaligned.txt: 32-byte windows
+// +20-30 % for binary64, -25 % for binary32 whose selects then dominate).
+// TFB_RS_MISLD overrides for tuning builds: 0 = 16-byte, 2 = 32-byte windows.
+#ifndef TFB_RS_MISLD
+#define TFB_RS_MISLD (-1)
+#endif
+template <typename T>
+__host__ __device__ constexpr int mis_ld_kind() {
+  return TFB_RS_MISLD >= 0 ? TFB_RS_MISLD : (sizeof(T) == 8 ? 2 : 0);
+}
+
+// Five 16-byte vectors of the row starting at the aligned vector holding element p[0]
+// (misaligned by m elements): three 32-byte loads (LDG.E.256, whole sectors) at the
+// 32-byte boundary below, then the 16-byte half is chosen per row.  Only 32-byte
+// blocks holding one of the `rem` row elements from p are read.
+template <typename T>
+__device__ __forceinline__ void window32(const T* p, int m, int64_t rem, typename Vec<T>::type (&out)[5]) {
+  using VT = typename Vec<T>::type;
+  constexpr int V = Vec<T>::V;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const int mv = (a & 16u) ? 1 : 0;  // p's 16-byte vector is the upper half of its 32-byte block
+  const VT* base = reinterpret_cast<const VT*>(a & ~uintptr_t(31));
+  VT c[6];
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    const int64_t first = int64_t(2 * i) * V - (mv * V + m);  // element index (from p) of the block's start
+    if (first < rem && (i < 2 || mv * V + m > 0)) {
+      ld_stream32(base + 2 * i, c[2 * i], c[2 * i + 1]);
+    } else {
+      c[2 * i] = VT{};
+      c[2 * i + 1] = VT{};
+    }
+  }
+#pragma unroll
+  for (int w = 0; w < 5; ++w) out[w] = mv ? c[w + 1] : c[w];
+}
+
 // One 16-byte vector through a chain (elements in order).
 template <int M, typename T, bool DOT>
 __device__ __forceinline__ void chain_vec(Pair<typename Acc<M, T>::type>& st, const typename Vec<T>::type& a,
@@ -174,13 +212,18 @@ __global__ void TFB_RS_BOUNDS rows_short_kernel(
           for (int h = 0; h < 2; ++h) {
             if (!whole && int64_t(4 * h) * V >= rem) break;
             VT a[5], b[5];
+            if constexpr (mis_ld_kind<T>() == 2) {
+              window32<T>(xr + e0 + int64_t(4 * h) * V, mx, rem - int64_t(4 * h) * V, a);
+              if constexpr (DOT) window32<T>(yr + e0 + int64_t(4 * h) * V, my, rem - int64_t(4 * h) * V, b);
+            } else {
 #pragma unroll
-            for (int w = 0; w < 5; ++w) {
-              const int64_t fx = int64_t(4 * h + w) * V - mx;  // first element of the vector
-              a[w] = (w < 4 || mx) && fx < rem ? __ldg(xa + 4 * h + w) : VT{};
-              if constexpr (DOT) {
-                const int64_t fy = int64_t(4 * h + w) * V - my;
-                b[w] = (w < 4 || my) && fy < rem ? __ldg(ya + 4 * h + w) : VT{};
+              for (int w = 0; w < 5; ++w) {
+                const int64_t fx = int64_t(4 * h + w) * V - mx;  // first element of the vector
+                a[w] = (w < 4 || mx) && fx < rem ? __ldg(xa + 4 * h + w) : VT{};
+                if constexpr (DOT) {
+                  const int64_t fy = int64_t(4 * h + w) * V - my;
+                  b[w] = (w < 4 || my) && fy < rem ? __ldg(ya + 4 * h + w) : VT{};
+                }
               }
             }
             T fa[5 * V], fb[5 * V];

@@ -880,12 +880,16 @@ def test_wrappers_accept_strided_numpy_lists_and_views(tfb, oracle, cuda):
 
 def test_host_rows_engine_equals_device_rows(tfb, oracle, cuda):
     """tf_host_reduce_rows (row blocks staged + overlapped, pitched DMA for pinned strided
-    input) == tf_reduce_rows on the device copy, bit for bit; many blocks via 1 MiB slots."""
+    input) == tf_reduce_rows on the device copy, bit for bit; many blocks via 1 MiB slots.
+    Rows longer than a slot (300_001 f64 / 600_001 f32 elements > 1 MiB) stream through
+    leaf-aligned chunks one row at a time (never size the slots to a whole row)."""
     from paper_1401_0248_b200 import _lib
     L = _lib.lib()
     eng = _lib.host_engine(0, chunk_bytes=1 << 20, threads=3)
     for dt, code in ((np.float32, 0), (np.float64, 1)):
-        for rows, cols, ld in ((37, 70_001, 70_001), (9, 4_999, 5_000), (300, 1_000, 1_003), (2, 3, 3)):
+        long_cols = 300_001 if dt == np.float64 else 600_001
+        for rows, cols, ld in ((37, 70_001, 70_001), (9, 4_999, 5_000), (300, 1_000, 1_003), (2, 3, 3),
+                               (3, long_cols, long_cols), (3, long_cols, long_cols + 3)):
             base = oracle.lcg_fill("mmix", rows * ld, 121, dt, True).reshape(rows, ld)
             ybase = oracle.lcg_fill("nr", rows * ld, 122, dt, True).reshape(rows, ld)
             want = {}
