@@ -671,17 +671,27 @@ def run_ours(args):
         if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
+        eng = None if rows else _tl.host_engine(local)
+        split = [0, 0]  # elements the GPU / the host workers reduced over the timed e2e steps
         w0 = time.perf_counter()
         with torch.cuda.nvtx.range("bench: e2e steps"):
             for _ in range(ke):
                 e2e_step()
+                if eng is not None:
+                    g_el, h_el = _tl.host_split(eng)
+                    split[0] += g_el
+                    split[1] += h_el
             torch.cuda.synchronize()
         wall = time.perf_counter() - w0
         if use_dist:
             tw = torch.tensor([wall], dtype=torch.float64, device=dev)
             dist.all_reduce(tw, op=dist.ReduceOp.MAX)
             wall = tw.item()
-        e2e = {"value": total_elems * ke / wall / 1e9, "unit": UNIT, "h2d_bytes_per_step": bytes_per_step,
+        # bytes that crossed the link: the GPU's share (the hybrid host path reduces the rest
+        # of the host-resident shard on the engine's host workers and uploads leaf pairs only)
+        gpu_frac = split[0] / max(1, split[0] + split[1]) if eng is not None else 1.0
+        h2d = int(round(bytes_per_step * gpu_frac))
+        e2e = {"value": total_elems * ke / wall / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 16 if not rows else cfg.rows * item,
                "steps": ke, "ms_per_step": 1e3 * wall / ke,
                "path": (("paper_1401_0248_b200.dot_rows(pinned host matrices) -> C-ABI tf_host_reduce_rows "
@@ -689,27 +699,31 @@ def run_ours(args):
                          "stream, overlapped with the row kernels; row pairs stored into mapped host memory")
                         if rows else
                         ("paper_1401_0248_b200.sharded_run(pinned host shard) -> C-ABI tf_host_reduce (host-buffer "
-                         "engine): leaf-aligned 16 MiB chunks DMA'd straight from the pinned shard on a copy stream, "
-                         "overlapped with the leaf kernels; tree kernel stores the pair into mapped host memory"
+                         "engine, hybrid): the GPU pipeline takes leaf-aligned 16 MiB chunks from the front of the shard "
+                         "(DMA'd straight from pinned memory on a copy stream, overlapped with the leaf kernels) while "
+                         "the engine's host workers reduce full leaves from the back with the same chains and leaf "
+                         "tree (csrc/hostleaf.cpp) and upload only their leaf pairs; one tree kernel over all leaf "
+                         "pairs stores the pair into mapped host memory (bit-identical to the device-resident result)"
                          + ("; NCCL all-gather + merge across ranks" if world > 1 else ""))),
+               "host_share": (split[1] / max(1, split[0] + split[1])) if eng is not None else 0.0,
                "timing": "wall clock around the steps after synchronize, max over ranks",
                **({"host_placement": numa} if numa else {})}
         # The link the e2e path streams over: plain pinned H2D of the same host
         # buffer (up to 1 GiB, best of 3, CUDA events) — the e2e ceiling.
         src = xh.view(-1).view(torch.uint8)[: 1 << 30]
         dst = torch.empty_like(src, device=dev)
-        h2d = 0.0
+        h2d_link = 0.0
         for _ in range(3):
             c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             c0.record()
             dst.copy_(src, non_blocking=True)
             c1.record()
             torch.cuda.synchronize()
-            h2d = max(h2d, src.numel() / (c0.elapsed_time(c1) * 1e-3) / 1e9)
+            h2d_link = max(h2d_link, src.numel() / (c0.elapsed_time(c1) * 1e-3) / 1e9)
         del dst, src, xh, yh
         _release_pinned(torch)
-        e2e["h2d_link_gbs"] = h2d
-        e2e["frac_of_h2d_link"] = (bytes_per_step / (1e-3 * e2e["ms_per_step"]) / 1e9) / h2d
+        e2e["h2d_link_gbs"] = h2d_link
+        e2e["frac_of_h2d_link"] = (e2e["h2d_bytes_per_step"] / (1e-3 * e2e["ms_per_step"]) / 1e9) / h2d_link
 
     # --- CPU baseline (rank 0, N=1 only): the reference arm's own routine -----
     cpu = None

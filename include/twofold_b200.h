@@ -289,6 +289,23 @@ int tf_host_engine_threads(const void* engine);
 int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const void* hy, int64_t n,
                    int leaf_log2, void* out_pair_host, void* after_stream);
 
+/* Hybrid host path of tf_host_reduce (1-D host operands, methods 0..4, no
+ * TwoProduct, inputs >= min_bytes per operand): the engine's host workers
+ * reduce full leaves from the back of the array while the GPU pipeline takes
+ * chunks from the front; the host leaf pairs are uploaded and one tf_merge_tree
+ * closes the tree — bit-identical to tf_reduce for every split.  threads: the
+ * number of host workers (0 = GPU only; < 0 keeps the current pool).  Defaults
+ * at creation: TFB_HYBRID_THREADS (all cores but one), TFB_HYBRID_MIN_MB (64). */
+int tf_host_engine_hybrid(void* engine, int threads, size_t min_bytes);
+/* Elements the last tf_host_reduce on this engine reduced on the GPU (these
+ * crossed the link) and on the host workers. */
+int tf_host_engine_last_split(const void* engine, int64_t* gpu_elems, int64_t* host_elems);
+/* The host workers' leaf reducer itself (no GPU needed): pairs of the full
+ * leaves [leaf_lo, leaf_hi) of x (and y) at leaf size 2^leaf_log2 (0 = auto for
+ * n), exactly the device leaves' pairs (tf_reduce_leaves).  Methods 0..4. */
+int tf_host_leaves(int method, int dtype, const void* x, const void* y, int64_t n, int leaf_log2, int64_t leaf_lo,
+                   int64_t leaf_hi, void* out_pairs);
+
 /* Row-wise form (tf_reduce_rows on host matrices): rows x cols with leading
  * dimensions ldx / ldy (elements); out_pairs_host: rows (value, error) pairs.
  * Row blocks are packed into the staging slots (pitched DMA for page-locked

@@ -68,6 +68,9 @@ def _bind(L):
         "tf_host_engine_threads": ([vp], i32),
         "tf_host_reduce": ([vp, i32, i32, vp, vp, i64, i32, vp, vp], i32),
         "tf_host_reduce_rows": ([vp, i32, i32, vp, vp, i64, i64, i64, i64, i32, vp, vp], i32),
+        "tf_host_engine_hybrid": ([vp, i32, sz], i32),
+        "tf_host_engine_last_split": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
+        "tf_host_leaves": ([i32, i32, vp, vp, i64, i32, i64, i64, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -124,6 +127,13 @@ def ensure_canary(device_index: int) -> None:
 
 _engines: dict = {}
 _default_engines: dict = {}
+
+
+def host_split(engine) -> tuple[int, int]:
+    """(elements the GPU reduced, elements the host workers reduced) in the engine's last call."""
+    a, b = ctypes.c_int64(0), ctypes.c_int64(0)
+    check(lib().tf_host_engine_last_split(engine, ctypes.byref(a), ctypes.byref(b)), "tf_host_engine_last_split")
+    return a.value, b.value
 
 
 def host_engine(device_index: int, chunk_bytes: int | None = None, threads: int | None = None):

@@ -26,12 +26,15 @@
 // Calls on one engine are serialised by its mutex; the call blocks until the
 // pair is in out_pair_host.
 #include <cuda_runtime.h>
+#include <xmmintrin.h>
 
 #include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -132,6 +135,68 @@ class CopyPool {
   size_t bytes_ = 0;
 };
 
+// Workers for the hybrid host path: start(job) runs job(worker) on every worker
+// asynchronously (the calling thread keeps driving the GPU pipeline); wait()
+// returns when all have finished.  Idle workers sleep on a condvar (no spin).
+// Each worker clears FTZ/DAZ once: subnormals are in contract.
+class LeafPool {
+ public:
+  explicit LeafPool(int workers) {
+    for (int i = 0; i < workers; ++i) workers_.emplace_back([this, i] { run(i); });
+  }
+  ~LeafPool() {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  int size() const { return static_cast<int>(workers_.size()); }
+  void start(std::function<void(int)> job) {
+    {
+      std::lock_guard<std::mutex> g(m_);
+      job_ = std::move(job);
+      pending_ = size();
+      ++gen_;
+    }
+    cv_.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+  }
+
+ private:
+  void run(int i) {
+    _mm_setcsr(_mm_getcsr() & ~0x8040u);  // FTZ (bit 15) and DAZ (bit 6) off
+    uint64_t seen = 0;
+    for (;;) {
+      std::function<void(int)> job;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        job = job_;
+      }
+      job(i);
+      {
+        std::lock_guard<std::mutex> g(m_);
+        if (--pending_ == 0) done_.notify_all();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  std::function<void(int)> job_;
+  uint64_t gen_ = 0;
+  int pending_ = 0;
+  bool stop_ = false;
+};
+
 struct DeviceGuard {
   int prev = -1;
   explicit DeviceGuard(int dev) {
@@ -180,6 +245,11 @@ struct HostEngine {
   void* counters = nullptr;
   int64_t counters_len = 0;
   CopyPool* pool = nullptr;
+  LeafPool* leaf_pool = nullptr;   // hybrid host path workers (nullptr: GPU only)
+  size_t hybrid_min_bytes = 0;     // per operand; smaller host inputs stay GPU-only
+  void* hpairs = nullptr;          // pinned: leaf pairs the host workers computed
+  size_t hpairs_bytes = 0;
+  int64_t last_gpu_elems = 0, last_cpu_elems = 0;  // split of the last host-path call
   std::mutex mu;
 };
 
@@ -207,6 +277,8 @@ void release(HostEngine* g) {
   if (g->stream) cudaStreamDestroy(g->stream);
   if (g->cstream) cudaStreamDestroy(g->cstream);
   delete g->pool;
+  delete g->leaf_pool;
+  if (g->hpairs) cudaFreeHost(g->hpairs);
   delete g;
 }
 
@@ -365,6 +437,141 @@ int staged_reduce(HostEngine* g, int method, int dtype, const char* cx, const ch
   if (rc == TF_OK) rc = cu(cudaStreamSynchronize(g->cstream));
   return rc;
 }
+
+extern "C" int tfb_host_leaves_avx512(int, int, const void*, const void*, int, int64_t, int64_t, void*);
+extern "C" int tfb_host_leaves_base(int, int, const void*, const void*, int, int64_t, int64_t, void*);
+
+int host_leaves(int method, int dtype, const void* x, const void* y, int lg, int64_t lo, int64_t hi, void* pairs) {
+  // TFB_HOSTLEAF_BASE=1 forces the x86-64 baseline build (tests: both builds give the same bits)
+  static const bool avx512 = !getenv("TFB_HOSTLEAF_BASE") && __builtin_cpu_supports("avx512f") &&
+                             __builtin_cpu_supports("avx512vl") && __builtin_cpu_supports("avx512dq");
+  return avx512 ? tfb_host_leaves_avx512(method, dtype, x, y, lg, lo, hi, pairs)
+                : tfb_host_leaves_base(method, dtype, x, y, lg, lo, hi, pairs);
+}
+
+bool hybrid_applies(const HostEngine* g, int method, int dtype, int64_t n, int lg, size_t item) {
+  if (!g->leaf_pool || g->leaf_pool->size() == 0) return false;
+  if (method & TF_TRACK_PRODUCT) return false;  // TwoProduct dots stay on the device
+  if (method < 0 || method > TF_KAHAN || (method == TF_WIDE && dtype != TF_F32)) return false;
+  if (lg < (dtype == TF_F64 ? 9 : 10)) return false;
+  return static_cast<size_t>(n) * item >= g->hybrid_min_bytes && (n >> lg) >= 2;
+}
+
+// The hybrid host path: the GPU pipeline claims chunks of full leaves from the
+// FRONT of the array while the leaf workers claim blocks of full leaves from the
+// BACK (work stealing, no calibration); they meet wherever the two rates put
+// them.  The host pairs are uploaded into their leaf slots, the partial last
+// leaf (if any) is reduced on the GPU, and tf_merge_tree builds the one balanced
+// tree over all leaf pairs — bit-identical to tf_reduce for every split.
+int hybrid_reduce(HostEngine* g, int method, int dtype, const char* cx, const char* cy, int64_t n, int lg, Mem kx,
+                  Mem ky, void* out) {
+  Range range("hybrid_reduce");
+  const size_t pair_bytes = pair_size(method, dtype);
+  const size_t item = dtype == TF_F64 ? 8 : 4;
+  const bool dot = cy != nullptr;
+  const int64_t L = int64_t(1) << lg;
+  const int64_t P = (n + L - 1) / L;
+  const int64_t Pfull = n / L;
+  size_t pb = 0;
+  int64_t cnt = 0, leaves = 0;
+  int rc = tf_workspace_size(method, dtype, 1, n, lg, &pb, &cnt, &leaves);
+  if (rc) return rc;
+  if ((rc = ensure_scratch(g, std::max<size_t>(pb, P * pair_bytes), std::max<int64_t>(cnt, 1)))) return rc;
+  if ((rc = grow_slots(g, std::max(std::min(static_cast<size_t>(n) * item, g->chunk_target),
+                                    static_cast<size_t>(L) * item))))
+    return rc;
+  if (static_cast<size_t>(P) * pair_bytes > g->hpairs_bytes) {
+    if ((rc = cu(cudaStreamSynchronize(g->stream)))) return rc;
+    if (g->hpairs) cudaFreeHost(g->hpairs);
+    g->hpairs = nullptr;
+    g->hpairs_bytes = 0;
+    if ((rc = cu(cudaHostAlloc(&g->hpairs, P * pair_bytes, cudaHostAllocDefault)))) return rc;
+    g->hpairs_bytes = P * pair_bytes;
+  }
+  const int64_t chunk_leaves = std::max<int64_t>(1, static_cast<int64_t>(g->chunk / (L * item)));
+  // host block: ~4 MiB per operand (a few leaves), so the two sides meet finely
+  const int64_t host_block = std::max<int64_t>(1, static_cast<int64_t>((size_t(4) << 20) / (L * item)));
+  std::mutex cm;
+  int64_t front = 0, back = Pfull;  // GPU owns [0, front), host owns [back, Pfull)
+  std::atomic<int> host_rc{0};
+  char* hp = static_cast<char*>(g->hpairs);
+  g->leaf_pool->start([&](int) {
+    for (;;) {
+      int64_t lo, hi;
+      {
+        std::lock_guard<std::mutex> lk(cm);
+        if (back <= front) return;
+        hi = back;
+        lo = std::max(front, back - host_block);
+        back = lo;
+      }
+      if (host_leaves(method, dtype, cx, cy, lg, lo, hi, hp + lo * pair_bytes) != 0) host_rc.store(-1);
+    }
+  });
+  // GPU side: chunks from the front; a chunk is claimed only when a staging slot
+  // is free (host wait), so the device never runs ahead of the link
+  int64_t c = 0;
+  for (;; ++c) {
+    int64_t lo, hi;
+    const int b = static_cast<int>(c & 1);
+    if (c >= 2 && (rc = cu(cudaEventSynchronize(g->k_done[b])))) break;
+    {
+      std::lock_guard<std::mutex> lk(cm);
+      if (front >= back) break;
+      lo = front;
+      hi = std::min(back, front + chunk_leaves);
+      front = hi;
+    }
+    Range r("gpu chunk");
+    const size_t bytes = static_cast<size_t>(hi - lo) * L * item;
+    if ((rc = stage(g, g->cstream, b, 0, cx + lo * L * item, bytes, kx, false))) break;
+    if (dot && (rc = stage(g, g->cstream, b, 1, cy + lo * L * item, bytes, ky, false))) break;
+    if ((rc = cu(cudaEventRecord(g->h2d_done[b], g->cstream)))) break;
+    if ((rc = cu(cudaStreamWaitEvent(g->stream, g->h2d_done[b], 0)))) break;
+    rc = tf_reduce_leaves(method, dtype, g->dev[b], dot ? g->dev[b] + g->chunk : nullptr, (hi - lo) * L, lg,
+                          static_cast<char*>(g->partials) + lo * pair_bytes, g->stream);
+    if (rc == TF_OK) rc = cu(cudaEventRecord(g->k_done[b], g->stream));
+    if (rc) break;
+  }
+  if (rc) {  // stop the workers' claims, let them drain, then fail
+    {
+      std::lock_guard<std::mutex> lk(cm);
+      back = front;
+    }
+    g->leaf_pool->wait();
+    cudaStreamSynchronize(g->cstream);
+    cudaStreamSynchronize(g->stream);
+    return rc;
+  }
+  // the partial last leaf, if any: one more (small) GPU chunk
+  if (Pfull < P) {
+    const int b = static_cast<int>(c & 1);
+    if (c >= 2 && (rc = cu(cudaEventSynchronize(g->k_done[b])))) return rc;
+    const int64_t m = n - Pfull * L;
+    if ((rc = stage(g, g->cstream, b, 0, cx + Pfull * L * item, m * item, kx, false))) return rc;
+    if (dot && (rc = stage(g, g->cstream, b, 1, cy + Pfull * L * item, m * item, ky, false))) return rc;
+    if ((rc = cu(cudaEventRecord(g->h2d_done[b], g->cstream)))) return rc;
+    if ((rc = cu(cudaStreamWaitEvent(g->stream, g->h2d_done[b], 0)))) return rc;
+    rc = tf_reduce_leaves(method, dtype, g->dev[b], dot ? g->dev[b] + g->chunk : nullptr, m, lg,
+                          static_cast<char*>(g->partials) + Pfull * pair_bytes, g->stream);
+    if (rc == TF_OK) rc = cu(cudaEventRecord(g->k_done[b], g->stream));
+    if (rc) return rc;
+  }
+  g->leaf_pool->wait();
+  if (host_rc.load()) return TF_EINVAL_ARG;
+  const int64_t host_lo = front;  // == back after both sides stopped
+  if (host_lo < Pfull &&
+      (rc = cu(cudaMemcpyAsync(static_cast<char*>(g->partials) + host_lo * pair_bytes, hp + host_lo * pair_bytes,
+                               static_cast<size_t>(Pfull - host_lo) * pair_bytes, cudaMemcpyHostToDevice,
+                               g->stream))))
+    return rc;
+  if ((rc = tf_merge_tree(method, dtype, g->partials, P, out, g->stream))) return rc;
+  if ((rc = cu(cudaStreamSynchronize(g->stream)))) return rc;
+  if ((rc = cu(cudaStreamSynchronize(g->cstream)))) return rc;
+  g->last_cpu_elems = (Pfull - host_lo) * L;
+  g->last_gpu_elems = n - g->last_cpu_elems;
+  return TF_OK;
+}
 }  // namespace
 }  // namespace tfb
 
@@ -412,6 +619,16 @@ int tf_host_engine_create(int device, int threads, size_t chunk_bytes, void** en
     return rc;
   }
   g->pool = new tfb::CopyPool(threads - 1);
+  // hybrid host path: all cores but the caller's by default (TFB_HYBRID_THREADS,
+  // 0 = GPU only), for host inputs >= TFB_HYBRID_MIN_MB (default 64) per operand
+  {
+    const char* e = getenv("TFB_HYBRID_THREADS");
+    int ht = e ? atoi(e) : -1;
+    if (ht < 0) ht = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()) - 1);
+    const char* mb = getenv("TFB_HYBRID_MIN_MB");
+    g->hybrid_min_bytes = (mb ? static_cast<size_t>(atoll(mb)) : size_t(64)) << 20;
+    g->leaf_pool = ht > 0 ? new tfb::LeafPool(ht) : nullptr;
+  }
   *engine = g;
   return TF_OK;
 }
@@ -431,6 +648,42 @@ int tf_host_engine_destroy(void* engine) {
 
 int tf_host_engine_threads(const void* engine) {
   return engine ? static_cast<const HostEngine*>(engine)->pool->threads() : 0;
+}
+
+int tf_host_engine_hybrid(void* engine, int threads, size_t min_bytes) {
+  if (!engine) return TF_EINVAL_ARG;
+  auto* g = static_cast<HostEngine*>(engine);
+  std::lock_guard<std::mutex> lk(g->mu);
+  if (threads >= 0) {
+    delete g->leaf_pool;
+    g->leaf_pool = threads > 0 ? new tfb::LeafPool(threads) : nullptr;
+  }
+  g->hybrid_min_bytes = min_bytes;
+  return TF_OK;
+}
+
+int tf_host_engine_last_split(const void* engine, int64_t* gpu_elems, int64_t* host_elems) {
+  if (!engine || !gpu_elems || !host_elems) return TF_EINVAL_ARG;
+  const auto* g = static_cast<const HostEngine*>(engine);
+  *gpu_elems = g->last_gpu_elems;
+  *host_elems = g->last_cpu_elems;
+  return TF_OK;
+}
+
+int tf_host_leaves(int method, int dtype, const void* x, const void* y, int64_t n, int leaf_log2, int64_t leaf_lo,
+                   int64_t leaf_hi, void* out_pairs) {
+  if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
+  if (method < 0 || method > TF_KAHAN) return TF_EINVAL_METHOD;
+  if (method == TF_WIDE && dtype != TF_F32) return TF_EINVAL_DTYPE;
+  if (n < 0) return TF_EINVAL_SHAPE;
+  const int lg = leaf_log2 ? leaf_log2 : tf_leaf_log2(dtype, n);
+  if (lg < (dtype == TF_F64 ? 9 : 10) || lg > 24) return TF_EINVAL_ARG;
+  if (leaf_lo < 0 || leaf_hi < leaf_lo || (leaf_hi << lg) > n || !x || !out_pairs) return TF_EINVAL_ARG;
+  const unsigned old = _mm_getcsr();
+  _mm_setcsr(old & ~0x8040u);
+  const int rc = tfb::host_leaves(method, dtype, x, y, lg, leaf_lo, leaf_hi, out_pairs);
+  _mm_setcsr(old);
+  return rc ? TF_EINVAL_ARG : TF_OK;
 }
 
 int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const void* hy, int64_t n,
@@ -510,7 +763,13 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
       return TF_OK;
     }
   }
-  if ((rc = tfb::staged_reduce(g, method, dtype, cx, cy, n, lg, kx, ky, g->pair_pin))) return rc;
+  if (tfb::hybrid_applies(g, method, dtype, n, lg, item)) {
+    if ((rc = tfb::hybrid_reduce(g, method, dtype, cx, cy, n, lg, kx, ky, g->pair_pin))) return rc;
+  } else {
+    if ((rc = tfb::staged_reduce(g, method, dtype, cx, cy, n, lg, kx, ky, g->pair_pin))) return rc;
+    g->last_gpu_elems = n;
+    g->last_cpu_elems = 0;
+  }
   std::memcpy(out_pair_host, g->pair_pin, pair_bytes);
   return TF_OK;
 }

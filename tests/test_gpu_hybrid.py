@@ -1,0 +1,74 @@
+"""The hybrid host path of tf_host_reduce (csrc/host.cu hybrid_reduce + csrc/hostleaf.cpp):
+host workers reduce full leaves from the back while the GPU pipeline takes chunks from
+the front; the result must equal tf_reduce on the device copy bit for bit, for every
+method / precision / sum-dot, pinned and pageable operands, a partial last leaf, and
+whatever split the two sides' speeds produce (several reruns)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _hex(p):
+    return (float(p[0]).hex(), float(p[1]).hex())
+
+
+def test_hybrid_equals_device_reduce(cuda, oracle):
+    import paper_1401_0248_b200 as tfb
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    eng = _lib.host_engine(0, chunk_bytes=1 << 20, threads=2)
+    _lib.check(L.tf_host_engine_hybrid(eng, 4, 1 << 20), "tf_host_engine_hybrid")
+    host_seen = 0
+    try:
+        for dt, code in ((np.float32, 0), (np.float64, 1)):
+            tdt = torch.float32 if dt == np.float32 else torch.float64
+            for n in ((1 << 20) + 123, 1 << 21):
+                xh = oracle.lcg_fill("mmix", n, 31, dt, True)
+                yh = oracle.lcg_fill("nr", n, 32, dt, True)
+                xd, yd = torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda)
+                for m in ((0, 1, 2, 3, 4) if dt == np.float32 else (0, 2, 3, 4)):
+                    meth = list(tfb.Method)[m]
+                    for dot in (False, True):
+                        want = tfb.reduce(meth, xd, yd if dot else None).cpu().numpy()
+                        for pinned in (False, True):
+                            xs = torch.from_numpy(xh)
+                            ys = torch.from_numpy(yh)
+                            if pinned:
+                                xs, ys = xs.pin_memory(), ys.pin_memory()
+                            for _ in range(2):
+                                out = np.empty(2, np.float64 if (m == 1 or dt == np.float64) else dt)
+                                rc = L.tf_host_reduce(eng, m, code, xs.data_ptr(), ys.data_ptr() if dot else None, n, 0,
+                                                      out.ctypes.data, None)
+                                _lib.check(rc, "tf_host_reduce")
+                                assert _hex(out) == _hex(want), (dt, n, m, dot, pinned)
+                                gpu, host = _lib.host_split(eng)
+                                assert gpu + host == n and host % 1024 == 0
+                                host_seen += host
+                # TwoProduct dots stay on the device path (no host leaves) and still agree
+                want = tfb.reduce(tfb.Method.TWOFOLD_RIGOROUS, xd, yd, track_product=True).cpu().numpy()
+                out = np.empty(2, dt)
+                _lib.check(L.tf_host_reduce(eng, 3 | 0x100, code, xh.ctypes.data, yh.ctypes.data, n, 0,
+                                            out.ctypes.data, None), "tf_host_reduce TP")
+                assert _hex(out) == _hex(want) and _lib.host_split(eng)[1] == 0
+    finally:
+        L.tf_host_engine_hybrid(eng, 0, 1 << 62)
+    assert host_seen > 0, "the host workers never took a leaf"
+
+
+def test_hybrid_public_api_large_input(cuda, oracle):
+    """Through the public API (default engine, hybrid above 64 MiB per operand): a 2^24
+    binary64 numpy dot is the grid result bit for bit, and the host shared the work."""
+    import paper_1401_0248_b200 as tfb
+    from paper_1401_0248_b200 import _lib
+    n = 1 << 24
+    xh = oracle.philox_fill("uniform_sym", n, 4, 0, 0, np.float64, nthreads=8)
+    yh = oracle.philox_fill("uniform_sym", n, 4, 1, 0, np.float64, nthreads=8)
+    want = tfb.reduce(tfb.Method.TWOFOLD_FAST, torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda))
+    r = tfb.dot_twofold_fast(xh, yh, flavor="cuda")
+    assert (float(r.value).hex(), float(r.error).hex()) == _hex(want.cpu().numpy())
+    gpu, host = _lib.host_split(_lib.host_engine(torch.cuda.current_device()))
+    assert gpu + host == n and host > 0, (gpu, host)
+    assert (float(r.value).hex(), float(r.error).hex()) == _hex(oracle.emulate(2, xh, yh))
