@@ -730,7 +730,9 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         del copies, x, y
         torch.cuda.empty_cache()
-        cpu = cpu_measure(args.config, cfg, method_name, steps=5, warmup=1)
+        # the reference arm's own routine and statistic, over the run's K / W (each step a
+        # bounded sample; K capped so the leg stays within seconds)
+        cpu = cpu_measure(args.config, cfg, method_name, steps=min(args.steps, 20), warmup=min(args.warmup, 5))
 
     dtype_name = "f64" if item == 8 else "f32"
     line = {

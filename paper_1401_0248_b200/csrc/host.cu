@@ -610,7 +610,9 @@ int tf_host_engine_create(int device, int threads, size_t chunk_bytes, void** en
     step(cudaHostAlloc(reinterpret_cast<void**>(&g->pin[b]), 2 * g->chunk, cudaHostAllocDefault));
     step(cudaMalloc(reinterpret_cast<void**>(&g->dev[b]), 2 * g->chunk));
     step(cudaEventCreateWithFlags(&g->h2d_done[b], cudaEventDisableTiming));
-    step(cudaEventCreateWithFlags(&g->k_done[b], cudaEventDisableTiming));
+    // k_done is host-waited only by the hybrid path, whose caller should sleep (its core
+    // belongs to the host workers), not spin
+    step(cudaEventCreateWithFlags(&g->k_done[b], cudaEventDisableTiming | cudaEventBlockingSync));
   }
   step(cudaHostAlloc(&g->pair_pin, 16, cudaHostAllocMapped));
   step(cudaEventCreateWithFlags(&g->entry, cudaEventDisableTiming));
