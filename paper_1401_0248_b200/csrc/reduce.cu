@@ -875,6 +875,40 @@ static int launch_rows_short(const T* px, const T* py, int64_t ldx, int64_t ldy,
   return check_launch();
 }
 
+// Misaligned one-leaf rows whose x / y share the 32-byte class sequence: class-uniform
+// warps (rows.cuh rows_cls_kernel).  TFB_ROWS_CLS=0 disables it (A/B runs).
+static int rows_cls_enabled() {
+  static const int v = getenv("TFB_ROWS_CLS") ? atoi(getenv("TFB_ROWS_CLS")) : 1;
+  return v;
+}
+
+template <int M, typename T, bool DOT>
+static int launch_rows_cls(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
+                           int leaf_log2, void* out, cudaStream_t stream) {
+  using A = typename Acc<M, T>::type;
+  constexpr int V = Vec<T>::V;
+  auto kern = &rows_cls_kernel<M, T, DOT>;
+  const int g_log2 = rows_short_glog2(cols, V);
+  const int64_t K = (cols + int64_t(kThreads) * V - 1) / (int64_t(kThreads) * V);
+  TFB_CHECK(K <= (int64_t(1) << leaf_log2) / (int64_t(kThreads) * V));
+  const int64_t pitch = (ldx * int64_t(sizeof(T))) % 32;
+  int period = 1;
+  while ((pitch * period) % 32) period <<= 1;  // rows until the 32-byte offset repeats
+  constexpr int kBlock = TFB_RS_BLOCK;
+  const int64_t rows_per_cta = int64_t(kBlock / 32) * (32 >> g_log2);
+  const int64_t want = (rows + rows_per_cta - 1) / rows_per_cta + period;  // + a partial super-block
+  const int64_t slots =
+      static_cast<int64_t>(device_sms()) * occupancy_of(reinterpret_cast<const void*>(kern), kBlock);
+  const unsigned grid = static_cast<unsigned>(want < slots ? want : slots);
+  snprintf(g_last_launch, sizeof(g_last_launch),
+           "rows_cls_kernel<%s,%s,%s,win32> grid=%u block=%d rows=%lld cols=%lld lanes/row=%d period=%d leaf_log2=%d",
+           method_tag(M), sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", grid, kBlock,
+           static_cast<long long>(rows), static_cast<long long>(cols), 1 << g_log2, period, leaf_log2);
+  kern<<<grid, kBlock, 0, stream>>>(px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2, period,
+                                      static_cast<Pair<A>*>(out));
+  return check_launch();
+}
+
 template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1, int MS = 0>
 static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                             int leaf_log2, int64_t P, void* partials, void* counters, void* out, int fused,
@@ -956,6 +990,11 @@ static int launch_leaves(const void* x, const void* y, int64_t ldx, int64_t ldy,
       };
       if (vec && a32(x, ldx) && (!DOT || a32(y, ldy)))
         return launch_rows_short<M, T, DOT, 2>(px, py, ldx, ldy, rows, cols, leaf_log2, out, stream);
+      // misaligned, x and y on the same 32-byte class sequence: class-uniform warps
+      const bool same_cls = !DOT || (((reinterpret_cast<uintptr_t>(x) - reinterpret_cast<uintptr_t>(y)) & 31u) == 0 &&
+                                     ((ldx - ldy) * int64_t(sizeof(T))) % 32 == 0);
+      if (!vec && same_cls && rows_cls_enabled() && rk == 0 && rows_short_glog2(cols, Vec<T>::V) > 0)
+        return launch_rows_cls<M, T, DOT>(px, py, ldx, ldy, rows, cols, leaf_log2, out, stream);
       return vec ? launch_rows_short<M, T, DOT, 1>(px, py, ldx, ldy, rows, cols, leaf_log2, out, stream)
                  : launch_rows_short<M, T, DOT, 0>(px, py, ldx, ldy, rows, cols, leaf_log2, out, stream);
     }

@@ -277,6 +277,168 @@ __global__ void TFB_RS_BOUNDS rows_short_kernel(
   }
 }
 
+// Misaligned pitches, class-uniform warps (rows_cls_kernel).  Row r's lane blocks
+// all sit at the same offset MOFF (elements) past a 32-byte boundary — the row
+// start's offset, since blocks are 128 bytes apart — and that offset repeats
+// with period p = 32 / gcd(ld * sizeof T, 32) rows.  Warps are therefore given
+// rows of ONE residue class mod p (rows q, q + p, q + 2p, ... of a super-block),
+// so MOFF is warp-uniform and a compile-time constant after one switch: each
+// lane block is read with five 32-byte loads (LDG.E.256, whole sectors; the
+// window shared by the two halves loaded once) and its elements are picked by
+// compile-time register indices — no per-element selects.  Used when x and y
+// share the class sequence (same base offset and pitch mod 32 bytes, e.g. two
+// views of the same shape); the chains, their order and the tree are exactly
+// rows_short_kernel's, so the bits are too.
+#ifndef TFB_CLS_ALL
+#define TFB_CLS_ALL 0  // tuning builds: 1 = load the block's five windows before any chain step
+#endif
+template <int M, typename T, bool DOT, int MOFF>
+__device__ __forceinline__ void cls_rows_chains(Pair<typename Acc<M, T>::type> (&ch)[8], const T* xr, const T* yr,
+                                                int64_t cols, int K, int j) {
+  using VT = typename Vec<T>::type;
+  constexpr int V = Vec<T>::V;
+  constexpr int W = 32 / sizeof(T);  // elements per 32-byte window
+  constexpr int kChains = 8;
+  for (int k = 0; k < K; ++k) {
+    const int64_t e0 = (int64_t(k) * kThreads + kChains * j) * V;  // the lane's block: elements [e0, e0 + 8V)
+    if (e0 >= cols) break;
+    const int64_t rem = cols - e0;
+    const VT* base = reinterpret_cast<const VT*>(xr + e0 - MOFF);  // 32-byte aligned
+    const VT* ybase = DOT ? reinterpret_cast<const VT*>(yr + e0 - MOFF) : nullptr;
+    const bool whole = rem >= kChains * V;
+#if TFB_CLS_ALL
+    // all five windows first (more loads in flight), then both halves
+    VT za[10], zb[10];
+#pragma unroll
+    for (int wi = 0; wi < 5; ++wi) {
+      const int64_t first = int64_t(wi) * W - MOFF;
+      if ((wi < 4 || MOFF > 0) && first < rem) {
+        ld_stream32(base + 2 * wi, za[2 * wi], za[2 * wi + 1]);
+        if constexpr (DOT) ld_stream32(ybase + 2 * wi, zb[2 * wi], zb[2 * wi + 1]);
+      } else {
+        za[2 * wi] = za[2 * wi + 1] = VT{};
+        if constexpr (DOT) zb[2 * wi] = zb[2 * wi + 1] = VT{};
+      }
+    }
+    T ga[5 * W], gb[5 * W];
+#pragma unroll
+    for (int v = 0; v < 10; ++v)
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        ga[v * V + q] = vget(za[v], q);
+        if constexpr (DOT) gb[v * V + q] = vget(zb[v], q);
+      }
+#pragma unroll
+    for (int c = 0; c < kChains; ++c)
+#pragma unroll
+      for (int q = 0; q < V; ++q) {
+        if (!whole && int64_t(c) * V + q >= rem) continue;
+        if constexpr (DOT) accumulate<M, T, true>(ch[c], ga[MOFF + c * V + q], gb[MOFF + c * V + q]);
+        else accumulate<M, T, false>(ch[c], ga[MOFF + c * V + q], T(0));
+      }
+    (void)j;
+    continue;
+#endif
+    VT wa[6], wb[6];  // windows 2..4 of the previous half are reused: 0,1,2 | 2,3,4
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (!whole && int64_t(4 * h) * V >= rem) break;
+#pragma unroll
+      for (int w = (h == 0 ? 0 : 1); w < 3; ++w) {  // window index within the half: 2h + w
+        const int wi = 2 * h + w;
+        const int64_t first = int64_t(wi) * W - MOFF;  // block-relative element of the window's start
+        const bool need = (wi < 4 || MOFF > 0) && first < rem;
+        if (need) {
+          ld_stream32(base + 2 * wi, wa[2 * w], wa[2 * w + 1]);
+          if constexpr (DOT) ld_stream32(ybase + 2 * wi, wb[2 * w], wb[2 * w + 1]);
+        } else {
+          wa[2 * w] = wa[2 * w + 1] = VT{};
+          if constexpr (DOT) wb[2 * w] = wb[2 * w + 1] = VT{};
+        }
+      }
+      T fa[3 * W], fb[3 * W];
+#pragma unroll
+      for (int v = 0; v < 6; ++v)
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          fa[v * V + q] = vget(wa[v], q);
+          if constexpr (DOT) fb[v * V + q] = vget(wb[v], q);
+        }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int q = 0; q < V; ++q) {
+          if (!whole && int64_t(4 * h + c) * V + q >= rem) continue;
+          if constexpr (DOT) accumulate<M, T, true>(ch[4 * h + c], fa[MOFF + c * V + q], fb[MOFF + c * V + q]);
+          else accumulate<M, T, false>(ch[4 * h + c], fa[MOFF + c * V + q], T(0));
+        }
+      // window 2 of this half is window 0 of the next
+      wa[0] = wa[4];
+      wa[1] = wa[5];
+      if constexpr (DOT) {
+        wb[0] = wb[4];
+        wb[1] = wb[5];
+      }
+    }
+  }
+}
+
+template <int M, typename T, bool DOT>
+__global__ void TFB_RS_BOUNDS rows_cls_kernel(
+    const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
+    int K, int g_log2, int period, Pair<typename Acc<M, T>::type>* __restrict__ out) {
+  using A = typename Acc<M, T>::type;
+  constexpr int kChains = 8;
+  constexpr int W = 32 / sizeof(T);
+  const int lane = threadIdx.x & 31;
+  const int G = 1 << g_log2;
+  const int j = lane & (G - 1);
+  const int64_t groups = 32 >> g_log2;
+  const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  // slot s = (super-block s / p, class s % p); the warp's rows: q + p*i of the block
+  for (int64_t s = warp;; s += nwarps) {  // warp-uniform
+    const int64_t sb = s / period, q = s % period;
+    const int64_t rfirst = sb * period * groups + q;
+    if (sb * period * groups >= rows) break;
+    const int64_t r = rfirst + int64_t(period) * (lane >> g_log2);
+    const int moff = static_cast<int>((reinterpret_cast<uintptr_t>(x + rfirst * ldx) & 31u) / sizeof(T));
+    Pair<A> ch[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) ch[c] = zero_pair<A>();
+    if (r < rows) {
+      const T* xr = x + r * ldx;
+      const T* yr = DOT ? y + r * ldy : nullptr;
+      switch (moff) {  // warp-uniform
+#define TFB_CLS_CASE(O) \
+  case O:               \
+    if constexpr (O < W) cls_rows_chains<M, T, DOT, O>(ch, xr, yr, cols, K, j); \
+    break;
+        TFB_CLS_CASE(0) TFB_CLS_CASE(1) TFB_CLS_CASE(2) TFB_CLS_CASE(3)
+        TFB_CLS_CASE(4) TFB_CLS_CASE(5) TFB_CLS_CASE(6) TFB_CLS_CASE(7)
+#undef TFB_CLS_CASE
+        default: break;
+      }
+    }
+#pragma unroll
+    for (int w = 1; w < kChains; w <<= 1)
+#pragma unroll
+      for (int c = 0; c < kChains; c += 2 * w) ch[c] = merge<M, A>(ch[c], ch[c + w]);
+    Pair<A> st = ch[0];
+    for (int off = 1; off < G; off <<= 1) {
+      Pair<A> o;
+      o.s = __shfl_down_sync(0xffffffffu, st.s, off, G);
+      if constexpr (HasErr<M>::value) o.e = __shfl_down_sync(0xffffffffu, st.e, off, G);
+      else o.e = A(0);
+      if ((j & (2 * off - 1)) == 0) st = merge<M, A>(st, o);
+    }
+    if (j == 0 && r < rows) {
+      for (int lv = 3 + g_log2; lv < 8; ++lv) st = merge<M, A>(st, zero_pair<A>());
+      out[r] = st;
+    }
+  }
+}
+
 // Lanes per row: pow2ceil(ceil(chains holding data / 8)), chains = min(256, ceil(cols / V)).
 inline int rows_short_glog2(int64_t cols, int V) {
   int64_t chains = (cols + V - 1) / V;

@@ -15,7 +15,7 @@ wait
 for ((i = 0; i < ${#args[@]}; i += 2)); do
   name=${args[i]}
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o build/variants/libtfb_$name.so \
-    build/variants/reduce_$name.o build/misc.o build/exact.o build/host.o build/canary.o -Xlinker -z,defs -lpthread -ldl -lrt
+    build/variants/reduce_$name.o $(ls build/*.o | grep -v '/reduce.o$') -Xlinker -z,defs -lpthread -ldl -lrt
   rm -f build/variants/reduce_$name.o
 done
 ls build/variants

@@ -964,3 +964,42 @@ def test_non_finite_misaligned_views(tfb, oracle, cuda):
                 meth = list(tfb.Method)[m]
                 got = tfb.reduce(meth, xd[off:off + n], yd[off:off + n]).cpu().numpy()
                 _same_nf(got, oracle.emulate(m, xs, ys), (dt, off, m))
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_rows_class_uniform_kernel_matches_emulator(tfb, oracle, cuda, dt):
+    """Misaligned pitches on the class-uniform warps (rows_cls_kernel: rows of one 32-byte
+    offset class per warp, 32-byte windows, compile-time element picks) == the emulator's
+    per-row tree, for every offset class, partial last blocks, sums and dots, and several
+    periods (pitch mod 32 bytes); x / y on different class sequences take the select path."""
+    L = tfb._lib.lib()
+    item = np.dtype(dt).itemsize
+    for cols, pad, off in ((777, 0, 1), (255, 2, 3), (17, 0, 1), (63, 1, 2), (1001, 0, 0), (130, 3, 1)):
+        rows = 203
+        ld = cols + pad
+        if (ld * item) % 16 == 0 and off * item % 16 == 0:
+            continue  # aligned: not this kernel
+        bx = oracle.lcg_fill("mmix", rows * ld + 8, 71 + cols, dt, True)
+        by = oracle.lcg_fill("nr", rows * ld + 8, 72 + cols, dt, True)
+        bx[5 * ld + 3] = -0.0
+        X = torch.from_numpy(bx).to(cuda)[off:off + rows * ld].view(rows, ld)[:, :cols]
+        Y = torch.from_numpy(by).to(cuda)[off:off + rows * ld].view(rows, ld)[:, :cols]
+        Xh, Yh = np.ascontiguousarray(X.cpu().numpy()), np.ascontiguousarray(Y.cpu().numpy())
+        for m in _methods(dt):
+            meth = list(tfb.Method)[m]
+            for yy, yyh in ((None, None), (Y, Yh)):
+                got = tfb.reduce_rows(meth, X, yy).cpu().numpy()
+                desc = L.tf_last_launch().decode()
+                if cols <= 1024 and cols * item > 128:  # one-lane rows (<= 8 vectors) keep element loads
+                    assert "rows_cls_kernel" in desc, desc
+                ev, ee = oracle.emulate_rows(m, Xh, yyh)
+                for r in range(rows):
+                    _same(got[r], (ev[r], ee[r]), (dt, cols, pad, off, m, r, yy is None))
+        # y on another class sequence (offset differs by one element): the select path, same bits
+        Y2 = torch.from_numpy(by).to(cuda)[off + 1:off + 1 + rows * ld].view(rows, ld)[:, :cols]
+        Y2h = np.ascontiguousarray(Y2.cpu().numpy())
+        got = tfb.reduce_rows(tfb.Method.TWOFOLD_FAST, X, Y2).cpu().numpy()
+        assert "rows_cls_kernel" not in L.tf_last_launch().decode()
+        ev, ee = oracle.emulate_rows(2, Xh, Y2h)
+        for r in range(rows):
+            _same(got[r], (ev[r], ee[r]), (dt, cols, "y other class", r))
