@@ -228,6 +228,13 @@ def bind_to_gpu_numa(local: int) -> str | None:
     return None
 
 
+def _numa_nodes() -> int:
+    try:
+        return max(1, len([d for d in os.listdir("/sys/devices/system/node") if d.startswith("node")]))
+    except OSError:
+        return 1
+
+
 def measured_peak():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
@@ -477,6 +484,12 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     numa = bind_to_gpu_numa(local) if world > 1 else None
+    if world > 1 and "TFB_HYBRID_THREADS" not in os.environ:
+        # the ranks of a node share its host cores: give each rank's hybrid host workers
+        # its share of the CPUs it may run on (NUMA-local after the binding above)
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+        os.environ["TFB_HYBRID_THREADS"] = str(max(1, len(os.sched_getaffinity(0))
+                                                   // max(1, local_world // max(1, _numa_nodes())) - 1))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1 or args.force_collective:

@@ -26,6 +26,7 @@
 // Calls on one engine are serialised by its mutex; the call blocks until the
 // pair is in out_pair_host.
 #include <cuda_runtime.h>
+#include <sched.h>
 #include <xmmintrin.h>
 
 #include <algorithm>
@@ -626,7 +627,13 @@ int tf_host_engine_create(int device, int threads, size_t chunk_bytes, void** en
   {
     const char* e = getenv("TFB_HYBRID_THREADS");
     int ht = e ? atoi(e) : -1;
-    if (ht < 0) ht = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()) - 1);
+    if (ht < 0) {  // the CPUs this process may run on (its affinity mask), minus the caller's
+      cpu_set_t set;
+      CPU_ZERO(&set);
+      const int n = sched_getaffinity(0, sizeof(set), &set) == 0 ? CPU_COUNT(&set)
+                                                                  : static_cast<int>(std::thread::hardware_concurrency());
+      ht = std::max(1, n) - 1;
+    }
     const char* mb = getenv("TFB_HYBRID_MIN_MB");
     g->hybrid_min_bytes = (mb ? static_cast<size_t>(atoll(mb)) : size_t(64)) << 20;
     g->leaf_pool = ht > 0 ? new tfb::LeafPool(ht) : nullptr;
