@@ -722,6 +722,8 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
   // Device or page-locked operands may still be in flight on the caller's
   // stream (NULL = the legacy default stream): order the engine's streams after it.
   if ((rc = tfb::after_caller(g, kx, ky, after_stream))) return rc;
+  g->last_gpu_elems = n;  // every path below but the hybrid one reduces everything on the GPU
+  g->last_cpu_elems = 0;
   if (kx == tfb::Mem::kDevice && ky == tfb::Mem::kDevice) {  // already resident: plain tf_reduce
     rc = tf_reduce(method, dtype, hx, hy, n, leaf_log2, g->pair_pin, g->partials, g->partials_bytes,
                    g->counters, g->counters_len, g->stream);
@@ -776,8 +778,6 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
     if ((rc = tfb::hybrid_reduce(g, method, dtype, cx, cy, n, lg, kx, ky, g->pair_pin))) return rc;
   } else {
     if ((rc = tfb::staged_reduce(g, method, dtype, cx, cy, n, lg, kx, ky, g->pair_pin))) return rc;
-    g->last_gpu_elems = n;
-    g->last_cpu_elems = 0;
   }
   std::memcpy(out_pair_host, g->pair_pin, pair_bytes);
   return TF_OK;
