@@ -295,7 +295,7 @@ int tf_host_reduce(void* engine, int method, int dtype, const void* hx, const vo
  * chunks from the front; the host leaf pairs are uploaded and one tf_merge_tree
  * closes the tree — bit-identical to tf_reduce for every split.  threads: the
  * number of host workers (0 = GPU only; < 0 keeps the current pool).  Defaults
- * at creation: TFB_HYBRID_THREADS (all cores but one), TFB_HYBRID_MIN_MB (64). */
+ * at creation: TFB_HYBRID_THREADS (the process's CPUs but one), TFB_HYBRID_MIN_MB (8). */
 int tf_host_engine_hybrid(void* engine, int threads, size_t min_bytes);
 /* Elements the last tf_host_reduce on this engine reduced on the GPU (these
  * crossed the link) and on the host workers. */

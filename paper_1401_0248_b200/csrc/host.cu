@@ -489,9 +489,14 @@ int hybrid_reduce(HostEngine* g, int method, int dtype, const char* cx, const ch
     if ((rc = cu(cudaHostAlloc(&g->hpairs, P * pair_bytes, cudaHostAllocDefault)))) return rc;
     g->hpairs_bytes = P * pair_bytes;
   }
-  const int64_t chunk_leaves = std::max<int64_t>(1, static_cast<int64_t>(g->chunk / (L * item)));
-  // host block: ~4 MiB per operand (a few leaves), so the two sides meet finely
-  const int64_t host_block = std::max<int64_t>(1, static_cast<int64_t>((size_t(4) << 20) / (L * item)));
+  // Claim granularity: GPU chunks of at most a slot and at most 1/8 of the leaves (a
+  // first chunk of half the array would leave the host idle), host blocks of at most
+  // 4 MiB per operand and small enough that every worker gets several.
+  const int64_t slot_leaves = std::max<int64_t>(1, static_cast<int64_t>(g->chunk / (L * item)));
+  const int64_t chunk_leaves = std::max<int64_t>(1, std::min(slot_leaves, (P + 7) / 8));
+  const int64_t workers = g->leaf_pool->size();
+  const int64_t host_block = std::max<int64_t>(
+      1, std::min(static_cast<int64_t>((size_t(4) << 20) / (L * item)), Pfull / (4 * workers)));
   std::mutex cm;
   int64_t front = 0, back = Pfull;  // GPU owns [0, front), host owns [back, Pfull)
   std::atomic<int> host_rc{0};
@@ -623,7 +628,7 @@ int tf_host_engine_create(int device, int threads, size_t chunk_bytes, void** en
   }
   g->pool = new tfb::CopyPool(threads - 1);
   // hybrid host path: all cores but the caller's by default (TFB_HYBRID_THREADS,
-  // 0 = GPU only), for host inputs >= TFB_HYBRID_MIN_MB (default 64) per operand
+  // 0 = GPU only), for host inputs >= TFB_HYBRID_MIN_MB (default 8) per operand
   {
     const char* e = getenv("TFB_HYBRID_THREADS");
     int ht = e ? atoi(e) : -1;
@@ -635,7 +640,7 @@ int tf_host_engine_create(int device, int threads, size_t chunk_bytes, void** en
       ht = std::max(1, n) - 1;
     }
     const char* mb = getenv("TFB_HYBRID_MIN_MB");
-    g->hybrid_min_bytes = (mb ? static_cast<size_t>(atoll(mb)) : size_t(64)) << 20;
+    g->hybrid_min_bytes = (mb ? static_cast<size_t>(atoll(mb)) : size_t(8)) << 20;
     g->leaf_pool = ht > 0 ? new tfb::LeafPool(ht) : nullptr;
   }
   *engine = g;

@@ -59,7 +59,7 @@ def test_hybrid_equals_device_reduce(cuda, oracle):
 
 
 def test_hybrid_public_api_large_input(cuda, oracle):
-    """Through the public API (default engine, hybrid above 64 MiB per operand): a 2^24
+    """Through the public API (default engine, hybrid above 8 MiB per operand): a 2^24
     binary64 numpy dot is the grid result bit for bit, and the host shared the work."""
     import paper_1401_0248_b200 as tfb
     from paper_1401_0248_b200 import _lib
