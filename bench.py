@@ -478,12 +478,14 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
+    rank, world, local = dist_env()
+    numa = bind_to_gpu_numa(local) if world > 1 else None
+    torch.cuda.set_device(local)  # before the package import runs its device canary
+
     import paper_1401_0248_b200 as tfb
     from paper_1401_0248_b200 import _lib as _tl
     from paper_1401_0248_b200.gen import CONFIGS, make_inputs
 
-    rank, world, local = dist_env()
-    numa = bind_to_gpu_numa(local) if world > 1 else None
     if world > 1 and "TFB_HYBRID_THREADS" not in os.environ:
         # the ranks of a node share its host cores: give each rank's hybrid host workers
         # its share of the CPUs it may run on (NUMA-local after the binding above)

@@ -76,11 +76,18 @@ def _import_canary() -> None:
     CUDA device nothing can run (every compute call raises), so there is
     nothing to check until one is visible; ensure_canary also runs per device
     on first use."""
+    import os
+
     import torch
 
     from . import _lib
     if torch.cuda.is_available():
-        _lib.ensure_canary(torch.cuda.current_device())
+        # under torchrun each rank owns GPU LOCAL_RANK: check that one rather than
+        # creating a context on device 0 in every rank
+        local = os.environ.get("LOCAL_RANK")
+        dev = int(local) if local is not None and local.isdigit() and int(local) < torch.cuda.device_count() \
+            else torch.cuda.current_device()
+        _lib.ensure_canary(dev)
 
 
 _import_canary()
