@@ -447,6 +447,10 @@ __global__ void TFB_LDG_BOUNDS(NT, UF) leaves_kernel(
   const int R = (1 << leaf_log2) / (kThreads * V);
   const int64_t per_row = P * S;
   const int64_t units = rows * per_row;
+  // Launched as a programmatic dependent of the previous kernel in the stream
+  // (launch_leaves_nt): resident early, but no memory access before that grid has
+  // completed and flushed — so any predecessor, ours or the caller's, is safe.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // partials-only mode may feed a programmatic-dependent tree kernel: let it be
   // scheduled now (it waits on griddepcontrol.wait for this grid's completion)
   if (!fused) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -505,6 +509,9 @@ __global__ void __launch_bounds__(kThreads) rows_tree_kernel(const Pair<A>* __re
                                                              uint32_t epoch) {
   __shared__ Pair<A> smem[kWarps];
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // the next kernel of the stream (e.g. the next call's leaves) may become resident now;
+  // it waits for this grid's completion before touching memory
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   TFB_CHECK(rows * per_row <= part_cap);
   for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
     Pair<A> root = tree_over<M, A>(partials + r * per_row, per_row, smem);
@@ -811,13 +818,16 @@ static int launch_small(const T* px, const T* py, int64_t n, int64_t P, void* ou
   cfg.gridDim = dim3(static_cast<unsigned>(C));
   cfg.blockDim = dim3(kThreads);
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  static const bool chain = !getenv("TFB_PDL_CHAIN") || atoi(getenv("TFB_PDL_CHAIN")) != 0;
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(C);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // see launch_leaves_nt
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = chain ? 2 : 1;
   snprintf(g_last_launch, sizeof(g_last_launch),
            "small_cluster_kernel<%s,%s,%s,%s> grid=%d cluster=%d block=%d leaves=%lld", method_tag(M),
            sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", VEC ? "ldg128" : "scalar", C, C, kThreads,
@@ -924,9 +934,23 @@ static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, 
            sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum",
            VEC ? "ldg128" : (MS ? (MS == 1 ? "ldg128-shift1" : MS == 2 ? "ldg128-shift2" : "ldg128-shift3") : "scalar"),
            NT, Unroll<T>::value * UF, grid, NT, static_cast<long long>(units), leaf_log2);
-  leaves_kernel<M, T, DOT, VEC, NT, UF, MS><<<grid, NT, 0, stream>>>(
-      px, py, ldx, ldy, rows, cols, leaf_log2, P, static_cast<Pair<A>*>(partials),
-      static_cast<unsigned*>(counters), static_cast<Pair<A>*>(out), fused, part_cap);
+  // programmatic dependent of the previous kernel (the kernel waits before any memory
+  // access): a preceding tree kernel's trigger lets these CTAs become resident before it
+  // retires, hiding the launch gap between back-to-back calls.  TFB_PDL_CHAIN=0 disables.
+  static const bool chain = !getenv("TFB_PDL_CHAIN") || atoi(getenv("TFB_PDL_CHAIN")) != 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = chain ? 1 : 0;
+  if (cudaLaunchKernelEx(&cfg, leaves_kernel<M, T, DOT, VEC, NT, UF, MS>, px, py, ldx, ldy, rows, cols, leaf_log2, P,
+                         static_cast<Pair<A>*>(partials), static_cast<unsigned*>(counters),
+                         static_cast<Pair<A>*>(out), fused, part_cap) != cudaSuccess)
+    return record_cuda_error();
   return check_launch();
 }
 

@@ -51,6 +51,10 @@ __global__ void __launch_bounds__(kThreads) small_cluster_kernel(const T* __rest
   TFB_CHECK(C <= kSmallMaxCluster && int64_t(C) * G >= P && gridDim.x == static_cast<unsigned>(C));
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int gsz = static_cast<int>(P2 < G ? P2 : G);  // leaves of this CTA's subtree
+  // programmatic dependent of the previous kernel (no memory access before it retired),
+  // and itself lets the next kernel of the stream become resident early
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   // ---- loads of every chain first (one round trip), then the recurrences ----
   VT a[G], b[G];
