@@ -45,3 +45,13 @@ def test_reference_arm_contract(cuda):
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "Gelem/s"
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
     assert d["cpu_baseline"]["value"] == d["value"] and d["cpu_baseline"]["kind"] in ("port", "reference")
+
+
+def test_self_launch_through_torchrun_with_the_collective(cuda):
+    """--gpus 1 --spawn re-executes under torch.distributed.run; --force-collective runs the
+    NCCL all-gather + merge kernel in every step at world size 1 (the N>1 code path)."""
+    d = _run("--gpus", "1", "--spawn", "--force-collective", "--config", "cfg5-weak", "--steps", "3", "--warmup", "3",
+             "--no-cpu", "--no-e2e")
+    assert d["n_gpus"] == 1 and d["value"] > 100 and "NCCL" in d["run"]["combine"]
+    assert d["roofline"]["kernel_ms"] <= d["ms_per_step"] * 1.001
+    assert d["config"]["n_per_rank"] == 1 << 29 and d["scaling"] == "weak"
