@@ -604,6 +604,7 @@ __global__ void __launch_bounds__(kThreads) noread_kernel(const T* __restrict__ 
 #include "small.cuh"
 #include "rows.cuh"
 #include "seqpipe.cuh"
+#include "seqsplit.cuh"
 namespace tfb {
 
 // ---------------------------------------------------------------------------
@@ -1139,9 +1140,47 @@ static int launch_seq_pipe(const void* x, const void* y, int64_t n, int k, void*
   return check_launch();
 }
 
+// seq flavor with the s / e chains decoupled (seqsplit.cuh): direct, wide, fast and
+// rigorous, no TwoProduct; same preconditions as the bulk-copy ring.  TFB_SEQ_SPLIT=0
+// keeps seq_pipe_kernel (A/B runs).
+template <int M, typename T, bool DOT>
+static int launch_seq_split(const void* x, const void* y, int64_t n, void* out, cudaStream_t s) {
+  using A = typename Acc<M, T>::type;
+  static const bool on = !getenv("TFB_SEQ_SPLIT") || atoi(getenv("TFB_SEQ_SPLIT")) != 0;
+  if constexpr (M == kKahan || is_tp<M>()) {
+    return -1;
+  } else {
+    constexpr int64_t CE = SplitSmem<M, T, DOT>::CE;
+    const uintptr_t mx = reinterpret_cast<uintptr_t>(x) & 15u;
+    if (!on || n < 4 * CE || (DOT && (reinterpret_cast<uintptr_t>(y) & 15u) != mx)) return -1;
+    const int64_t head = static_cast<int64_t>((16u - mx) & 15u) / static_cast<int64_t>(sizeof(T));
+    const int64_t nchunks = (n - head) / CE;
+    auto kern = &seq_split_kernel<M, T, DOT>;
+    const size_t smem = SplitSmem<M, T, DOT>::kBytes;
+    static std::mutex mu;
+    static std::unordered_map<int, bool> ok;
+    {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      std::lock_guard<std::mutex> g(mu);
+      if (!ok.count(dev)) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+            cudaSuccess)
+          return record_cuda_error();
+        ok[dev] = true;
+      }
+    }
+    kern<<<1, kSplitThreads, smem, s>>>(static_cast<const T*>(x), static_cast<const T*>(y), n, head, nchunks,
+                                         static_cast<Pair<A>*>(out));
+    return check_launch();
+  }
+}
+
 template <int M, typename T, bool DOT>
 static int launch_seq(const void* x, const void* y, int64_t n, void* out, cudaStream_t s) {
   using A = typename Acc<M, T>::type;
+  const int rs = launch_seq_split<M, T, DOT>(x, y, n, out, s);
+  if (rs >= 0) return rs;
   const int rc = launch_seq_pipe<M, T, DOT>(x, y, n, 1, out, s);
   if (rc >= 0) return rc;
   seq_kernel<M, T, DOT><<<1, 1, 0, s>>>(static_cast<const T*>(x), static_cast<const T*>(y), n,
