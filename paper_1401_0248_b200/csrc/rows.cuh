@@ -409,6 +409,10 @@ __global__ void TFB_RS_BOUNDS rows_cls_kernel(
     if (r < rows) {
       const T* xr = x + r * ldx;
       const T* yr = DOT ? y + r * ldy : nullptr;
+      // the warp's rows share one 32-byte offset class (x and y alike): the premise of
+      // the compile-time picks (debug builds assert it)
+      TFB_CHECK(static_cast<int>((reinterpret_cast<uintptr_t>(xr) & 31u) / sizeof(T)) == moff);
+      TFB_CHECK(!DOT || static_cast<int>((reinterpret_cast<uintptr_t>(yr) & 31u) / sizeof(T)) == moff);
       switch (moff) {  // warp-uniform
 #define TFB_CLS_CASE(O) \
   case O:               \
