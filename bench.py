@@ -759,7 +759,7 @@ def run_ours(args):
         "run": {"l2": (f"rotating over {R} input copies ({R * bytes_per_step / 1e6:.0f} MB >= 4x the 126 MB L2)"
                        if R > 1 else f"inputs {bytes_per_step / 2**30:.1f} GiB per rank >> 126 MB L2 (no flush)"),
                 "leaf_log2": (leaf_arg if not rows else
-                              (args.leaf_log2 or tfb.leaf_log2_for(x_dtype_of(cfg), cfg.rows * cfg.cols))),
+                              (args.leaf_log2 or tfb.leaf_log2_for(cfg.dtype, cfg.rows * cfg.cols))),
                 "steps_timing": "CUDA graph replay" if use_graph else "eager launches",
                 "steps_timed": K_eff, "n_this_rank": n,
                 **({"combine": combine_desc} if world > 1 or args.force_collective else {})},
@@ -780,20 +780,15 @@ def run_ours(args):
     return 0
 
 
-def x_dtype_of(cfg):
-    return cfg.dtype
-
-
 def _release_pinned(torch) -> None:
     """Return the caching host allocator's pinned blocks to the OS (the e2e shard
     can be 64 GiB; the CPU baseline allocates its own pageable sample next)."""
-    for fn in ("_host_emptyCache",):
-        f = getattr(torch._C, fn, None)
-        if f is not None:
-            try:
-                f()
-            except Exception:
-                pass
+    f = getattr(torch._C, "_host_emptyCache", None)
+    if f is not None:
+        try:
+            f()
+        except Exception:
+            pass
 
 
 def _reserve_stdout():
