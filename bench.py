@@ -686,7 +686,7 @@ def run_ours(args):
         if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
-        eng = None if rows else _tl.host_engine(local)
+        eng = _tl.host_engine(local)
         split = [0, 0]  # elements the GPU / the host workers reduced over the timed e2e steps
         w0 = time.perf_counter()
         with torch.cuda.nvtx.range("bench: e2e steps"):
@@ -704,14 +704,16 @@ def run_ours(args):
             wall = tw.item()
         # bytes that crossed the link: the GPU's share (the hybrid host path reduces the rest
         # of the host-resident shard on the engine's host workers and uploads leaf pairs only)
-        gpu_frac = split[0] / max(1, split[0] + split[1]) if eng is not None else 1.0
+        gpu_frac = split[0] / max(1, split[0] + split[1])
         h2d = int(round(bytes_per_step * gpu_frac))
         e2e = {"value": total_elems * ke / wall / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": 16 if not rows else cfg.rows * item,
                "steps": ke, "ms_per_step": 1e3 * wall / ke,
                "path": (("paper_1401_0248_b200.dot_rows(pinned host matrices) -> C-ABI tf_host_reduce_rows "
-                         "(host-buffer engine): 16 MiB row blocks DMA'd straight from the pinned matrices on a copy "
-                         "stream, overlapped with the row kernels; row pairs stored into mapped host memory")
+                         "(host-buffer engine, hybrid): the GPU takes row blocks from the front (DMA'd straight from "
+                         "the pinned matrices on a copy stream, overlapped with the row kernels) while the engine's "
+                         "host workers reduce whole rows from the back with the same leaves and row tree "
+                         "(csrc/hostleaf.cpp); row pairs stored into mapped host memory")
                         if rows else
                         ("paper_1401_0248_b200.sharded_run(pinned host shard) -> C-ABI tf_host_reduce (host-buffer "
                          "engine, hybrid): the GPU pipeline takes leaf-aligned 16 MiB chunks from the front of the shard "
@@ -720,7 +722,7 @@ def run_ours(args):
                          "tree (csrc/hostleaf.cpp) and upload only their leaf pairs; one tree kernel over all leaf "
                          "pairs stores the pair into mapped host memory (bit-identical to the device-resident result)"
                          + ("; NCCL all-gather + merge across ranks" if world > 1 else ""))),
-               "host_share": (split[1] / max(1, split[0] + split[1])) if eng is not None else 0.0,
+               "host_share": split[1] / max(1, split[0] + split[1]),
                "timing": "wall clock around the steps after synchronize, max over ranks",
                **({"host_placement": numa} if numa else {})}
         # The link the e2e path streams over: plain pinned H2D of the same host

@@ -306,6 +306,13 @@ int tf_host_engine_last_split(const void* engine, int64_t* gpu_elems, int64_t* h
 int tf_host_leaves(int method, int dtype, const void* x, const void* y, int64_t n, int leaf_log2, int64_t leaf_lo,
                    int64_t leaf_hi, void* out_pairs);
 
+/* The host workers' row reducer (no GPU needed): pairs of rows [row_lo, row_hi)
+ * of a (rows, cols) matrix with leading dimensions ldx / ldy at the matrix's leaf
+ * size (0 = auto for rows * cols) — each row's leaves and row tree exactly as
+ * tf_reduce_rows.  Used by tf_host_reduce_rows' hybrid path.  Methods 0..4. */
+int tf_host_rows(int method, int dtype, const void* x, const void* y, int64_t rows, int64_t cols, int64_t ldx,
+                 int64_t ldy, int leaf_log2, int64_t row_lo, int64_t row_hi, void* out_pairs);
+
 /* Row-wise form (tf_reduce_rows on host matrices): rows x cols with leading
  * dimensions ldx / ldy (elements); out_pairs_host: rows (value, error) pairs.
  * Row blocks are packed into the staging slots (pitched DMA for page-locked

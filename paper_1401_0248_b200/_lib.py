@@ -71,6 +71,7 @@ def _bind(L):
         "tf_host_engine_hybrid": ([vp, i32, sz], i32),
         "tf_host_engine_last_split": ([vp, ctypes.POINTER(i64), ctypes.POINTER(i64)], i32),
         "tf_host_leaves": ([i32, i32, vp, vp, i64, i32, i64, i64, vp], i32),
+        "tf_host_rows": ([i32, i32, vp, vp, i64, i64, i64, i64, i32, i64, i64, vp], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

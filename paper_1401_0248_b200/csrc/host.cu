@@ -450,12 +450,28 @@ int host_leaves(int method, int dtype, const void* x, const void* y, int lg, int
                 : tfb_host_leaves_base(method, dtype, x, y, lg, lo, hi, pairs);
 }
 
-bool hybrid_applies(const HostEngine* g, int method, int dtype, int64_t n, int lg, size_t item) {
+extern "C" int tfb_host_rows_avx512(int, int, const void*, const void*, int64_t, int64_t, int64_t, int64_t, int64_t,
+                                    int, void*);
+extern "C" int tfb_host_rows_base(int, int, const void*, const void*, int64_t, int64_t, int64_t, int64_t, int64_t, int,
+                                  void*);
+
+int host_rows(int method, int dtype, const void* x, const void* y, int64_t lo, int64_t hi, int64_t cols, int64_t ldx,
+              int64_t ldy, int lg, void* pairs) {
+  static const bool avx512 = !getenv("TFB_HOSTLEAF_BASE") && __builtin_cpu_supports("avx512f") &&
+                             __builtin_cpu_supports("avx512vl") && __builtin_cpu_supports("avx512dq");
+  return avx512 ? tfb_host_rows_avx512(method, dtype, x, y, lo, hi, cols, ldx, ldy, lg, pairs)
+                : tfb_host_rows_base(method, dtype, x, y, lo, hi, cols, ldx, ldy, lg, pairs);
+}
+
+bool hybrid_methods(const HostEngine* g, int method, int dtype, int lg) {
   if (!g->leaf_pool || g->leaf_pool->size() == 0) return false;
   if (method & TF_TRACK_PRODUCT) return false;  // TwoProduct dots stay on the device
   if (method < 0 || method > TF_KAHAN || (method == TF_WIDE && dtype != TF_F32)) return false;
-  if (lg < (dtype == TF_F64 ? 9 : 10)) return false;
-  return static_cast<size_t>(n) * item >= g->hybrid_min_bytes && (n >> lg) >= 2;
+  return lg >= (dtype == TF_F64 ? 9 : 10);
+}
+
+bool hybrid_applies(const HostEngine* g, int method, int dtype, int64_t n, int lg, size_t item) {
+  return hybrid_methods(g, method, dtype, lg) && static_cast<size_t>(n) * item >= g->hybrid_min_bytes && (n >> lg) >= 2;
 }
 
 // The hybrid host path: the GPU pipeline claims chunks of full leaves from the
@@ -684,6 +700,22 @@ int tf_host_engine_last_split(const void* engine, int64_t* gpu_elems, int64_t* h
   return TF_OK;
 }
 
+int tf_host_rows(int method, int dtype, const void* x, const void* y, int64_t rows, int64_t cols, int64_t ldx,
+                 int64_t ldy, int leaf_log2, int64_t row_lo, int64_t row_hi, void* out_pairs) {
+  if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
+  if (method < 0 || method > TF_KAHAN) return TF_EINVAL_METHOD;
+  if (method == TF_WIDE && dtype != TF_F32) return TF_EINVAL_DTYPE;
+  if (rows < 0 || cols < 0 || (rows > 1 && (ldx < cols || (y && ldy < cols)))) return TF_EINVAL_SHAPE;
+  const int lg = leaf_log2 ? leaf_log2 : tf_leaf_log2(dtype, rows * cols);
+  if (lg < (dtype == TF_F64 ? 9 : 10) || lg > 24) return TF_EINVAL_ARG;
+  if (row_lo < 0 || row_hi < row_lo || row_hi > rows || (cols > 0 && !x) || !out_pairs) return TF_EINVAL_ARG;
+  const unsigned old = _mm_getcsr();
+  _mm_setcsr(old & ~0x8040u);
+  const int rc = tfb::host_rows(method, dtype, x, y, row_lo, row_hi, cols, ldx, ldy, lg, out_pairs);
+  _mm_setcsr(old);
+  return rc ? TF_EINVAL_ARG : TF_OK;
+}
+
 int tf_host_leaves(int method, int dtype, const void* x, const void* y, int64_t n, int leaf_log2, int64_t leaf_lo,
                    int64_t leaf_hi, void* out_pairs) {
   if (dtype != TF_F32 && dtype != TF_F64) return TF_EINVAL_DTYPE;
@@ -828,6 +860,8 @@ int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, con
   if (kx == tfb::Mem::kOtherDevice || ky == tfb::Mem::kOtherDevice) return TF_EINVAL_ARG;
   if ((rc = tfb::after_caller(g, kx, ky, after_stream))) return rc;
   const size_t row_bytes = static_cast<size_t>(cols) * item;
+  g->last_gpu_elems = rows * cols;
+  g->last_cpu_elems = 0;
   if (kx == tfb::Mem::kDevice && ky == tfb::Mem::kDevice) {
     rc = tf_reduce_rows(method, dtype, hx, hy, rows, cols, ldx, ldy, lg, g->rows_pin, g->partials,
                         g->partials_bytes, g->counters, g->counters_len, g->stream);
@@ -839,10 +873,19 @@ int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, con
     // bit-identical to tf_reduce_rows), instead of sizing the slots to a whole row.
     const auto* cx = static_cast<const char*>(hx);
     const auto* cy = static_cast<const char*>(hy);
-    for (int64_t r = 0; r < rows && rc == TF_OK; ++r)
-      rc = tfb::staged_reduce(g, method, dtype, cx + static_cast<size_t>(r) * ldx * item,
-                              dot ? cy + static_cast<size_t>(r) * ldy * item : nullptr, cols, lg, kx, ky,
-                              static_cast<char*>(g->rows_pin) + static_cast<size_t>(r) * pair_bytes);
+    const bool hyb = tfb::hybrid_applies(g, method, dtype, cols, lg, item);
+    int64_t gpu_el = 0, host_el = 0;
+    for (int64_t r = 0; r < rows && rc == TF_OK; ++r) {
+      const char* xr = cx + static_cast<size_t>(r) * ldx * item;
+      const char* yr = dot ? cy + static_cast<size_t>(r) * ldy * item : nullptr;
+      char* o = static_cast<char*>(g->rows_pin) + static_cast<size_t>(r) * pair_bytes;
+      rc = hyb ? tfb::hybrid_reduce(g, method, dtype, xr, yr, cols, lg, kx, ky, o)
+               : tfb::staged_reduce(g, method, dtype, xr, yr, cols, lg, kx, ky, o);
+      gpu_el += hyb ? g->last_gpu_elems : cols;
+      host_el += hyb ? g->last_cpu_elems : 0;
+    }
+    g->last_gpu_elems = gpu_el;
+    g->last_cpu_elems = host_el;
   } else {
     // Row blocks, packed (leading dimension = cols) into the staging slots; the
     // copies of block b+1 (copy stream) overlap the reduction of block b.
@@ -868,13 +911,52 @@ int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, con
       for (int64_t r = 0; r < nr; ++r) g->pool->copy(p + r * row_bytes, s0 + static_cast<size_t>(r) * ld * item, row_bytes);
       return tfb::cu(cudaMemcpyAsync(d, p, static_cast<size_t>(nr) * row_bytes, cudaMemcpyHostToDevice, g->cstream));
     };
-    for (int64_t c = 0; c < nblocks && rc == TF_OK; ++c) {
+    // Hybrid (as tf_host_reduce): the GPU claims row blocks from the front, the
+    // engine's host workers whole rows from the back (csrc/hostleaf.cpp row
+    // reducer: the same leaves and row tree), straight into the mapped row pairs.
+    const bool hybrid = tfb::hybrid_methods(g, method, dtype, lg) && rows >= 2 &&
+                        static_cast<size_t>(rows) * row_bytes >= g->hybrid_min_bytes;
+    std::mutex cm;
+    int64_t front = 0, back = rows;  // GPU owns [0, front), host owns [back, rows)
+    std::atomic<int> host_rc{0};
+    // everything the workers' lambda captures lives at this scope (they run until wait())
+    const int64_t workers = hybrid ? g->leaf_pool->size() : 1;
+    const int64_t hb = std::max<int64_t>(
+        1, std::min(static_cast<int64_t>((size_t(4) << 20) / std::max<size_t>(row_bytes, 1)), rows / (4 * workers)));
+    char* const rp = static_cast<char*>(g->rows_pin);
+    if (hybrid) {
+      g->leaf_pool->start([&](int) {
+        for (;;) {
+          int64_t lo, hi;
+          {
+            std::lock_guard<std::mutex> lk(cm);
+            if (back <= front) return;
+            hi = back;
+            lo = std::max(front, back - hb);
+            back = lo;
+          }
+          if (tfb::host_rows(method, dtype, cx, cy, lo, hi, cols, ldx, ldy, lg, rp + lo * pair_bytes) != 0)
+            host_rc.store(-1);
+        }
+      });
+    }
+    const int64_t gblock = hybrid ? std::max<int64_t>(1, std::min(block, (rows + 7) / 8)) : block;
+    (void)nblocks;
+    for (int64_t c = 0; rc == TF_OK; ++c) {
       const int b = static_cast<int>(c & 1);
-      const int64_t r0 = c * block;
-      const int64_t nr = std::min(rows, r0 + block) - r0;
-      if (c >= 2 && (rc = tfb::cu(cudaStreamWaitEvent(g->cstream, g->k_done[b], 0)))) break;
-      if ((rc = stage_block(b, 0, cx, ldx, r0, nr, kx, c >= 2))) break;
-      if (dot && (rc = stage_block(b, 1, cy, ldy, r0, nr, ky, c >= 2))) break;
+      if (hybrid && c >= 2 && (rc = tfb::cu(cudaEventSynchronize(g->k_done[b])))) break;
+      int64_t r0, nr;
+      {
+        std::lock_guard<std::mutex> lk(cm);
+        if (front >= back) break;
+        r0 = front;
+        nr = std::min(back - front, gblock);
+        front += nr;
+      }
+      const bool wait = !hybrid && c >= 2;
+      if (wait && (rc = tfb::cu(cudaStreamWaitEvent(g->cstream, g->k_done[b], 0)))) break;
+      if ((rc = stage_block(b, 0, cx, ldx, r0, nr, kx, wait))) break;
+      if (dot && (rc = stage_block(b, 1, cy, ldy, r0, nr, ky, wait))) break;
       if ((rc = tfb::cu(cudaEventRecord(g->h2d_done[b], g->cstream)))) break;
       if ((rc = tfb::cu(cudaStreamWaitEvent(g->stream, g->h2d_done[b], 0)))) break;
       rc = tf_reduce_rows(method, dtype, g->dev[b], dot ? g->dev[b] + g->chunk : nullptr, nr, cols, cols, cols, lg,
@@ -882,6 +964,16 @@ int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, con
                           g->partials_bytes, g->counters, g->counters_len, g->stream);
       if (rc == TF_OK) rc = tfb::cu(cudaEventRecord(g->k_done[b], g->stream));
     }
+    if (hybrid) {
+      if (rc) {
+        std::lock_guard<std::mutex> lk(cm);
+        back = front;
+      }
+      g->leaf_pool->wait();
+      if (rc == TF_OK && host_rc.load()) rc = TF_EINVAL_ARG;
+    }
+    g->last_gpu_elems = front * cols;
+    g->last_cpu_elems = (rows - front) * cols;
   }
   if (rc) {
     cudaStreamSynchronize(g->cstream);

@@ -72,3 +72,41 @@ def test_hybrid_public_api_large_input(cuda, oracle):
     gpu, host = _lib.host_split(_lib.host_engine(torch.cuda.current_device()))
     assert gpu + host == n and host > 0, (gpu, host)
     assert (float(r.value).hex(), float(r.error).hex()) == _hex(oracle.emulate(2, xh, yh))
+
+
+def test_hybrid_rows_equal_device_rows(cuda, oracle):
+    """tf_host_reduce_rows' hybrid path (GPU row blocks from the front, host workers whole
+    rows from the back): every row pair == tf_reduce_rows on the device copy, one-leaf,
+    partial-leaf and multi-leaf rows, strided pitches, pinned and pageable."""
+    import paper_1401_0248_b200 as tfb
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    eng = _lib.host_engine(0, chunk_bytes=1 << 20, threads=2)
+    _lib.check(L.tf_host_engine_hybrid(eng, 4, 1 << 20), "tf_host_engine_hybrid")
+    host_seen = 0
+    try:
+        for dt, code in ((np.float32, 0), (np.float64, 1)):
+            for rows, cols, ld in ((512, 4096, 4096), (300, 5000, 5003), (24, 70_001, 70_001)):
+                X = oracle.lcg_fill("mmix", rows * ld, 41, dt, True).reshape(rows, ld)
+                Y = oracle.lcg_fill("nr", rows * ld, 42, dt, True).reshape(rows, ld)
+                Xd = torch.from_numpy(X).to(cuda)[:, :cols]
+                Yd = torch.from_numpy(Y).to(cuda)[:, :cols]
+                for m in ((0, 1, 2, 3, 4) if dt == np.float32 else (0, 2, 3, 4)):
+                    meth = list(tfb.Method)[m]
+                    for dot in (False, True):
+                        want = tfb.reduce_rows(meth, Xd, Yd if dot else None).cpu().numpy()
+                        for pinned in (False, True):
+                            xt, yt = torch.from_numpy(X), torch.from_numpy(Y)
+                            if pinned:
+                                xt, yt = xt.pin_memory(), yt.pin_memory()
+                            out = np.empty((rows, 2), np.float64 if (m == 1 or dt == np.float64) else dt)
+                            rc = L.tf_host_reduce_rows(eng, m, code, xt.data_ptr(), yt.data_ptr() if dot else None,
+                                                       rows, cols, ld, ld, 0, out.ctypes.data, None)
+                            _lib.check(rc, "tf_host_reduce_rows")
+                            assert out.tobytes() == want.tobytes(), (dt, rows, cols, m, dot, pinned)
+                            gpu, host = _lib.host_split(eng)
+                            assert gpu + host == rows * cols and host % cols == 0
+                            host_seen += host
+    finally:
+        L.tf_host_engine_hybrid(eng, 0, 1 << 62)
+    assert host_seen > 0

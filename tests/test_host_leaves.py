@@ -83,3 +83,38 @@ def test_baseline_build_gives_the_same_bits():
     runs = [subprocess.run([sys.executable, "-c", code % (repo, os.path.join(repo, "tests"))], env=dict(os.environ, **extra), capture_output=True,
                            text=True, check=True, cwd=repo).stdout for extra in ({}, {"TFB_HOSTLEAF_BASE": "1"})]
     assert runs[0] == runs[1] and len(runs[0]) > 1000
+
+
+def _host_rows(m, X, Y, lg, lo, hi, cols, ld):
+    L = _lib.lib()
+    dt = 0 if X.dtype == np.float32 else 1
+    acc = np.float64 if (m == 1 or dt == 1) else np.float32
+    out = np.zeros(2 * (hi - lo), acc)
+    rows = X.shape[0] if X.ndim == 2 else 1
+    rc = L.tf_host_rows(m, dt, X.ctypes.data, None if Y is None else Y.ctypes.data, rows, cols, ld, ld, lg, lo, hi,
+                        out.ctypes.data)
+    _lib.check(rc, "tf_host_rows")
+    return out[0::2], out[1::2]
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_host_rows_equal_device_rows(oracle, dt):
+    """The hybrid rows path's CPU row reducer == the emulator's per-row tree: one-leaf rows
+    (full and partial leaves), multi-leaf rows (leaf tree padded to a power of two, a
+    partial last leaf), strided leading dimensions, sums and dots, every method."""
+    rng = np.random.default_rng(11 if dt == np.float32 else 12)
+    lo_lg = 10 if dt == np.float32 else 9
+    for rows, cols, pad, lg in ((7, 1 << lo_lg, 0, lo_lg), (5, 777, 3, lo_lg), (4, 3 * (1 << lo_lg) + 5, 1, lo_lg),
+                                (6, 100, 0, lo_lg + 2), (3, 5 * (1 << lo_lg), 0, lo_lg), (2, 1, 0, lo_lg)):
+        ld = cols + pad
+        Xb = _data(rng, rows * ld, dt, "wide").reshape(rows, ld)
+        Yb = _data(rng, rows * ld, dt, "uniform").reshape(rows, ld)
+        Xc, Yc = np.ascontiguousarray(Xb[:, :cols]), np.ascontiguousarray(Yb[:, :cols])
+        for m in ((0, 1, 2, 3, 4) if dt == np.float32 else (0, 2, 3, 4)):
+            for yy, yyc in ((None, None), (Yb, Yc)):
+                ev, ee = oracle.emulate_rows(m, Xc, yyc, lg)
+                gs, ge = _host_rows(m, Xb, yy, lg, 0, rows, cols, ld)
+                assert gs.tobytes() == ev.astype(gs.dtype).tobytes(), (dt, rows, cols, pad, lg, m, yy is None)
+                assert ge.tobytes() == ee.astype(ge.dtype).tobytes(), (dt, rows, cols, pad, lg, m, yy is None)
+                s1, e1 = _host_rows(m, Xb, yy, lg, 1, rows, cols, ld)  # a sub-range of rows
+                assert s1.tobytes() == gs[1:].tobytes() and e1.tobytes() == ge[1:].tobytes()
