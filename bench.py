@@ -415,6 +415,23 @@ def cpu_measure(name: str, cfg, method: str, steps: int, warmup: int) -> dict:
             "cpu": cpu_model(), "thp": _thp()}
 
 
+def cpu_leg(args, steps: int, warmup: int) -> dict:
+    """cpu_baseline of our arm: run `bench.py --impl reference` (the reference arm) as a
+    child process on this config and K / W and take its cpu_baseline — one code path and
+    one kind of process for both CPU figures."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "LOCAL_WORLD_SIZE")}
+    env.update(TFB_BENCH_CHILD="1", CUDA_VISIBLE_DEVICES="")
+    cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--config", args.config,
+           "--steps", str(steps), "--warmup", str(warmup)]
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=1800)
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    if out.returncode != 0 or not lines:
+        raise RuntimeError(f"CPU reference leg failed: {out.stderr[-2000:]}")
+    cpu = json.loads(lines[-1])["cpu_baseline"]
+    cpu["sample"] += "; measured by the reference arm (bench.py --impl reference) in a child process"
+    return cpu
+
+
 # ---------------------------------------------------------------------------
 # Arms
 
@@ -422,6 +439,9 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    # the CPU arm never touches a GPU: hide them, so the package import creates no
+    # CUDA context (no driver threads or pinned pools beside the timed CPU work)
+    os.environ["CUDA_VISIBLE_DEVICES"] = ""
     from paper_1401_0248_b200.gen import CONFIGS
     cfg_key, method, _, _ = WORKLOADS[args.config]
     cfg = CONFIGS[cfg_key]
@@ -747,9 +767,9 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu:
         del copies, x, y
         torch.cuda.empty_cache()
-        # the reference arm's own routine and statistic, over the run's K / W (each step a
-        # bounded sample; K capped so the leg stays within seconds)
-        cpu = cpu_measure(args.config, cfg, method_name, steps=min(args.steps, 20), warmup=min(args.warmup, 5))
+        # the reference arm itself, in a fresh process (same routine, same process
+        # conditions as `--impl reference`), over the run's K / W (capped: seconds)
+        cpu = cpu_leg(args, steps=min(args.steps, 20), warmup=min(args.warmup, 5))
 
     dtype_name = "f64" if item == 8 else "f32"
     line = {
