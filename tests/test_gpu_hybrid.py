@@ -110,3 +110,38 @@ def test_hybrid_rows_equal_device_rows(cuda, oracle):
     finally:
         L.tf_host_engine_hybrid(eng, 0, 1 << 62)
     assert host_seen > 0
+
+
+def test_hybrid_fuzz_vs_emulator(cuda, oracle):
+    """Randomised hybrid calls (sizes, misaligned host views, pinned / pageable, methods,
+    precisions, sums / dots, explicit leaf sizes, 1..8 host workers) == the emulator."""
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    eng = _lib.host_engine(0, chunk_bytes=1 << 20, threads=2)
+    rng = np.random.default_rng(20261021)
+    try:
+        for case in range(60):
+            dt = np.float32 if rng.random() < 0.5 else np.float64
+            code = 0 if dt == np.float32 else 1
+            m = int(rng.choice((0, 1, 2, 3, 4) if dt == np.float32 else (0, 2, 3, 4)))
+            dot = bool(rng.random() < 0.6)
+            n = int(rng.integers(1 << 13, 1 << 21))
+            off = int(rng.integers(0, 4))
+            lo_lg = 10 if dt == np.float32 else 9
+            lg = int(rng.choice([0, 0, rng.integers(lo_lg, 15)]))
+            workers = int(rng.integers(1, 9))
+            _lib.check(L.tf_host_engine_hybrid(eng, workers, 1), "tf_host_engine_hybrid")
+            base_x = (rng.standard_normal(n + off) * 2.0 ** rng.integers(-20, 20, n + off)).astype(dt)
+            base_y = rng.uniform(-1, 1, n + off).astype(dt)
+            xt, yt = torch.from_numpy(base_x), torch.from_numpy(base_y)
+            if rng.random() < 0.5:
+                xt, yt = xt.pin_memory(), yt.pin_memory()
+            xs, ys = xt[off:], yt[off:]
+            out = np.empty(2, np.float64 if (m == 1 or dt == np.float64) else dt)
+            rc = L.tf_host_reduce(eng, m, code, xs.data_ptr(), ys.data_ptr() if dot else None, n, lg,
+                                  out.ctypes.data, None)
+            _lib.check(rc, "tf_host_reduce")
+            want = oracle.emulate(m, base_x[off:], base_y[off:] if dot else None, lg)
+            assert _hex(out) == _hex(want), (case, dt, m, dot, n, off, lg, workers)
+    finally:
+        L.tf_host_engine_hybrid(eng, 0, 1 << 62)
