@@ -145,3 +145,49 @@ def test_hybrid_fuzz_vs_emulator(cuda, oracle):
             assert _hex(out) == _hex(want), (case, dt, m, dot, n, off, lg, workers)
     finally:
         L.tf_host_engine_hybrid(eng, 0, 1 << 62)
+
+
+def test_hybrid_non_finite_matches_device(cuda, oracle):
+    """inf / -inf / NaN / overflowing entries on either side of the host / GPU split: the
+    hybrid pair == the device-resident pair (NaN matches NaN: payloads are not portable)."""
+    import math
+
+    import paper_1401_0248_b200 as tfb
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    eng = _lib.host_engine(0, chunk_bytes=1 << 20, threads=2)
+    _lib.check(L.tf_host_engine_hybrid(eng, 4, 1), "tf_host_engine_hybrid")
+    rng = np.random.default_rng(5)
+    try:
+        for dt, code in ((np.float32, 0), (np.float64, 1)):
+            n = 1 << 20
+            for pattern in ("inf_head", "inf_tail", "both", "nan", "ovf"):
+                x = rng.uniform(-1, 1, n).astype(dt)
+                y = rng.uniform(-1, 1, n).astype(dt)
+                big = np.finfo(dt).max
+                if pattern == "inf_head":
+                    x[17] = np.inf
+                elif pattern == "inf_tail":
+                    x[n - 100] = -np.inf
+                elif pattern == "both":
+                    x[3], x[n - 3] = np.inf, -np.inf
+                elif pattern == "nan":
+                    x[n // 2] = np.nan
+                else:
+                    x[n - 50:n - 47] = big
+                xd, yd = torch.from_numpy(x).to(cuda), torch.from_numpy(y).to(cuda)
+                for m in ((0, 1, 2, 3, 4) if dt == np.float32 else (0, 2, 3, 4)):
+                    for dot in (False, True):
+                        want = tfb.reduce(list(tfb.Method)[m], xd, yd if dot else None).cpu().numpy()
+                        out = np.empty(2, np.float64 if (m == 1 or dt == np.float64) else dt)
+                        with np.errstate(all="ignore"):
+                            _lib.check(L.tf_host_reduce(eng, m, code, x.ctypes.data, y.ctypes.data if dot else None,
+                                                        n, 0, out.ctypes.data, None), "tf_host_reduce")
+                        for g, w in zip(out, want):
+                            if math.isnan(float(w)):
+                                assert math.isnan(float(g)), (dt, pattern, m, dot, out, want)
+                            else:
+                                assert float(g).hex() == float(w).hex(), (dt, pattern, m, dot, out, want)
+                        assert _lib.host_split(eng)[1] > 0
+    finally:
+        L.tf_host_engine_hybrid(eng, 0, 1 << 62)
