@@ -109,6 +109,16 @@ int tf_set_leaf_split(int split);
  * the initial value. */
 int tf_set_tail(int tail);
 
+/* Tuning knob (process-wide): L2 prefetch preamble of the LDG leaves kernel.  The
+ * kernel is launched as a programmatic dependent of whatever precedes it in the
+ * stream; before it waits for that kernel's completion each CTA asks the L2 (bulk
+ * prefetch, a hint: nothing is read into the SM, and the L2 is the point of
+ * coherence) for the first `kib` KiB per operand of its first leaf, so HBM streams
+ * the head of this call while the predecessor's tail retires.  -1 = automatic
+ * (a 32 MiB budget shared by the grid), 0 = off, up to 512.  Result-neutral; env
+ * TFB_PF_KB sets the initial value. */
+int tf_set_prefetch(int kib);
+
 /* Tuning knob (process-wide): kernel for tf_reduce_rows when every row fits one
  * leaf (cols <= 2^leaf_log2) — 0 = automatic (rows of <= 16 KiB per operand: a
  * group of 1..32 lanes per row, rows.cuh; longer rows: one CTA per row), 1 =

@@ -42,6 +42,7 @@ def _bind(L):
         "tf_set_leaf_split": ([i32], i32),
         "tf_set_loader": ([i32], i32),
         "tf_set_tail": ([i32], i32),
+        "tf_set_prefetch": ([i32], i32),
         "tf_set_rows_kernel": ([i32], i32),
         "tf_last_launch": ([], ctypes.c_char_p),
         "tf_workspace_size": ([i32, i32, i64, i64, i32, ctypes.POINTER(sz), ctypes.POINTER(i64),

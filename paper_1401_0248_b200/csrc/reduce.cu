@@ -38,6 +38,24 @@ namespace tfb {
 constexpr int kThreads = 256;  // chains per leaf (the tree geometry) and default CTA size
 constexpr int kWarps = kThreads / 32;
 
+// Tuning builds only (-DTFB_TRACE, scripts/trace_cfg2.py): per-CTA %globaltimer stamps
+// of the leaves / tree kernels into a caller-provided buffer (tf_trace_buffer), 8 slots
+// per CTA; the tree kernel takes the record after the last CTA slot.
+#ifdef TFB_TRACE
+__device__ unsigned long long* tfb_trace_ptr = nullptr;
+__device__ __forceinline__ unsigned long long trace_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void trace_mark(unsigned rec, int slot) {
+  if (threadIdx.x == 0 && tfb_trace_ptr) tfb_trace_ptr[rec * 8ull + slot] = trace_now();
+}
+#define TFB_TR(rec, slot) trace_mark(rec, slot)
+#else
+#define TFB_TR(rec, slot)
+#endif
+
 template <typename T> struct Vec;
 template <> struct Vec<float> { using type = float4; static constexpr int V = 4; };
 template <> struct Vec<double> { using type = double2; static constexpr int V = 2; };
@@ -433,12 +451,41 @@ template <> struct Unroll<double> { static constexpr int value = TFB_UNROLL_F64;
 #else
 #define TFB_LDG_BOUNDS(NT, UF) __launch_bounds__(NT)
 #endif
+// Preamble of leaves_kernel, before the grid dependency resolves: ask the L2 for the head
+// of this CTA's first leaf (bulk prefetch — a hint that moves no data into the SM, and the
+// L2 is the point of coherence, so a predecessor still writing the operands is
+// unaffected).  When the call is queued behind another kernel, HBM streams the head while
+// that kernel's tail retires (launch_leaves_nt picks the size; 0 = off).  Not inlined: its
+// address arithmetic must not add to the streaming loop's register budget.
+template <typename T, bool DOT>
+__device__ __noinline__ void prefetch_first_leaf(const T* x, const T* y, int64_t ldx, int64_t ldy, int64_t cols,
+                                                 int leaf_log2, int64_t per_row, int64_t units, int pf_kb) {
+  if (pf_kb <= 0 || static_cast<int64_t>(blockIdx.x) >= units) return;
+  const int64_t r = blockIdx.x / per_row;
+  const int64_t start = (blockIdx.x - r * per_row) << leaf_log2;
+  int64_t bytes = cols - start < (int64_t(1) << leaf_log2) ? cols - start : (int64_t(1) << leaf_log2);
+  bytes *= static_cast<int64_t>(sizeof(T));
+  if (bytes > (static_cast<int64_t>(pf_kb) << 10)) bytes = static_cast<int64_t>(pf_kb) << 10;
+  bytes &= ~int64_t(15);
+  const int op = threadIdx.x & 1;
+  const int64_t off = static_cast<int64_t>(threadIdx.x >> 1) * 4096;
+  if (off < bytes && (DOT || op == 0)) {
+    const char* p = reinterpret_cast<const char*>((op ? y + r * ldy : x + r * ldx) + start) + off;
+    const unsigned sz = static_cast<unsigned>(bytes - off < 4096 ? bytes - off : 4096);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(sz) : "memory");
+  }
+}
+
+// leaves_kernel flags: bit 0 fused tail (retire ticket); bits 8.. KiB per operand of the
+// CTA's first leaf to prefetch into L2 before the dependency wait
+constexpr int kLeavesFused = 1;
+constexpr int kLeavesPrefetchShift = 8;
 template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1, int MS = 0>
 __global__ void TFB_LDG_BOUNDS(NT, UF) leaves_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy,
     int64_t rows, int64_t cols, int leaf_log2, int64_t P,
     Pair<typename Acc<M, T>::type>* __restrict__ partials, unsigned* __restrict__ counters,
-    Pair<typename Acc<M, T>::type>* __restrict__ out, int fused, int64_t part_cap) {
+    Pair<typename Acc<M, T>::type>* __restrict__ out, int flags, int64_t part_cap) {
   using A = typename Acc<M, T>::type;
   constexpr int V = Vec<T>::V;
   constexpr int S = kThreads / NT;
@@ -447,10 +494,22 @@ __global__ void TFB_LDG_BOUNDS(NT, UF) leaves_kernel(
   const int R = (1 << leaf_log2) / (kThreads * V);
   const int64_t per_row = P * S;
   const int64_t units = rows * per_row;
+  const int fused = flags & kLeavesFused;
+  TFB_TR(blockIdx.x, 0);
+#ifdef TFB_TRACE
+  if (threadIdx.x == 0 && tfb_trace_ptr) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    tfb_trace_ptr[blockIdx.x * 8ull + 4] = sm;
+  }
+#endif
+  if constexpr (VEC && S == 1)
+    prefetch_first_leaf<T, DOT>(x, y, ldx, ldy, cols, leaf_log2, per_row, units, flags >> kLeavesPrefetchShift);
   // Launched as a programmatic dependent of the previous kernel in the stream
   // (launch_leaves_nt): resident early, but no memory access before that grid has
   // completed and flushed — so any predecessor, ours or the caller's, is safe.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  TFB_TR(blockIdx.x, 1);
   // partials-only mode may feed a programmatic-dependent tree kernel: let it be
   // scheduled now (it waits on griddepcontrol.wait for this grid's completion)
   if (!fused) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -463,10 +522,12 @@ __global__ void TFB_LDG_BOUNDS(NT, UF) leaves_kernel(
     const T* yr = DOT ? y + r * ldy : nullptr;
     Pair<A> st = leaf_chain<M, T, DOT, VEC, Unroll<T>::value * UF, MS>(
         xr, yr, l << leaf_log2, cols, R, part * NT + static_cast<int>(threadIdx.x));
+    TFB_TR(blockIdx.x, 2);
     st = block_tree<M, A>(st, smem, NT);
     if (!fused) {
       TFB_CHECK(u < part_cap);
       if (threadIdx.x == 0) partials[u] = st;
+      TFB_TR(blockIdx.x, 3);
       continue;
     }
     if (per_row == 1) {
@@ -508,7 +569,9 @@ __global__ void __launch_bounds__(kThreads) rows_tree_kernel(const Pair<A>* __re
                                                              int64_t part_cap, const PeerCtx* __restrict__ peer,
                                                              uint32_t epoch) {
   __shared__ Pair<A> smem[kWarps];
+  TFB_TR(4096, 0);
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  TFB_TR(4096, 1);
   // the next kernel of the stream (e.g. the next call's leaves) may become resident now;
   // it waits for this grid's completion before touching memory
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -518,6 +581,7 @@ __global__ void __launch_bounds__(kThreads) rows_tree_kernel(const Pair<A>* __re
     finish_root<M, A>(root, out + r, peer, epoch, smem);
     __syncthreads();
   }
+  TFB_TR(4096, 2);
 }
 
 // Sequential flavor: the reference recurrence, one thread, left to right.
@@ -734,6 +798,40 @@ static int tail_choice() {
   return g_tail;
 }
 
+// L2 prefetch preamble of the LDG leaves kernel (result-neutral): KiB per operand of each
+// CTA's first leaf requested before the dependency wait.  -1 = automatic, 0 = off; env
+// TFB_PF_KB or tf_set_prefetch() choose.  Automatic (scripts/prefetch_sweep.py,
+// profiles/r02_prefetch_preamble.txt): a total budget shared by the grid's CTAs and
+// operands — more than the L2 can hold ahead of the demand stream costs re-reads.
+static int g_prefetch_kb = -2;
+static int prefetch_choice() {
+  if (g_prefetch_kb == -2) {
+    const char* e = getenv("TFB_PF_KB");
+    g_prefetch_kb = e ? atoi(e) : -1;
+    if (g_prefetch_kb < -1) g_prefetch_kb = -1;
+    if (g_prefetch_kb > 512) g_prefetch_kb = 512;
+  }
+  return g_prefetch_kb;
+}
+// Automatic size (measured, profiles/r02_prefetch_preamble.txt): inputs up to 8 MiB are
+// requested whole (the requests land before the dependency resolves); above, the grid
+// shares a budget of 0.3 x the input, at most 32 MiB — requests the L2 cannot complete
+// ahead of the demand stream compete with it (cfg2: 32 KiB per operand per CTA 22.0 us,
+// 64 KiB 25.1 us, off 24.1 us).
+static int prefetch_kb_for(unsigned grid, int operands, int64_t input_bytes) {
+  const int c = prefetch_choice();
+  if (c >= 0) return c;
+  int64_t budget = input_bytes;
+  if (input_bytes > (int64_t(8) << 20)) {
+    budget = input_bytes / 10 * 3;
+    if (budget < (int64_t(8) << 20)) budget = int64_t(8) << 20;
+    if (budget > (int64_t(32) << 20)) budget = int64_t(32) << 20;
+  }
+  int64_t kb = (budget / (int64_t(grid) * operands) + 1023) >> 10;
+  kb = (kb + 3) & ~int64_t(3);  // whole 4 KiB pieces, at least one
+  return static_cast<int>(kb > 512 ? 512 : kb);
+}
+
 template <int M, typename A>
 static int launch_rows_tree_pdl(const void* partials, int64_t rows, int64_t per_row, void* out,
                                 cudaStream_t stream, int64_t part_cap, const PeerCtx* peer, uint32_t epoch) {
@@ -833,7 +931,8 @@ static int launch_small(const T* px, const T* py, int64_t n, int64_t P, void* ou
            "small_cluster_kernel<%s,%s,%s,%s> grid=%d cluster=%d block=%d leaves=%lld", method_tag(M),
            sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", VEC ? "ldg128" : "scalar", C, C, kThreads,
            static_cast<long long>(P));
-  if (cudaLaunchKernelEx(&cfg, kern, px, py, n, P, P2, static_cast<Pair<A>*>(out)) != cudaSuccess)
+  if (cudaLaunchKernelEx(&cfg, kern, px, py, n, P, P2, static_cast<Pair<A>*>(out),
+                         chain && prefetch_choice() != 0 ? 1 : 0) != cudaSuccess)
     return record_cuda_error();
   return check_launch();
 }
@@ -948,9 +1047,14 @@ static int launch_leaves_nt(const T* px, const T* py, int64_t ldx, int64_t ldy, 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = chain ? 1 : 0;
+  const int flags = (fused ? kLeavesFused : 0) |
+                    ((chain && VEC && NT == kThreads
+                          ? prefetch_kb_for(grid, DOT ? 2 : 1, rows * cols * int64_t(sizeof(T)) * (DOT ? 2 : 1))
+                          : 0)
+                     << kLeavesPrefetchShift);
   if (cudaLaunchKernelEx(&cfg, leaves_kernel<M, T, DOT, VEC, NT, UF, MS>, px, py, ldx, ldy, rows, cols, leaf_log2, P,
                          static_cast<Pair<A>*>(partials), static_cast<unsigned*>(counters),
-                         static_cast<Pair<A>*>(out), fused, part_cap) != cudaSuccess)
+                         static_cast<Pair<A>*>(out), flags, part_cap) != cudaSuccess)
     return record_cuda_error();
   return check_launch();
 }
@@ -1302,6 +1406,12 @@ int tf_set_tail(int tail) {
   return TF_OK;
 }
 
+int tf_set_prefetch(int kib) {
+  if (kib < -1 || kib > 512) return TF_EINVAL_ARG;
+  g_prefetch_kb = kib;
+  return TF_OK;
+}
+
 int tf_set_loader(int loader) {
   if (loader < 0 || loader > 8 || loader == 4 || loader == 5) return TF_EINVAL_ARG;
   g_loader = loader;
@@ -1488,3 +1598,11 @@ int tf_reduce_lanes(int method, int dtype, const void* x, const void* y, int64_t
 }
 
 }  // extern "C"
+
+#ifdef TFB_TRACE
+// Tuning builds only: where the kernels' %globaltimer stamps go (device pointer, >= 8 * 4104 u64; null = off).
+extern "C" int tf_trace_buffer(void* dev_u64) {
+  unsigned long long* p = static_cast<unsigned long long*>(dev_u64);
+  return cudaMemcpyToSymbol(tfb::tfb_trace_ptr, &p, sizeof(p)) == cudaSuccess ? TF_OK : TF_ECUDA;
+}
+#endif

@@ -35,7 +35,8 @@ template <int M, typename T, bool DOT, bool VEC>
 __global__ void __launch_bounds__(kThreads) small_cluster_kernel(const T* __restrict__ x,
                                                                  const T* __restrict__ y, int64_t n,
                                                                  int64_t P, int64_t P2,
-                                                                 Pair<typename Acc<M, T>::type>* __restrict__ out) {
+                                                                 Pair<typename Acc<M, T>::type>* __restrict__ out,
+                                                                 int prefetch) {
   namespace cg = cooperative_groups;
   using A = typename Acc<M, T>::type;
   using VT = typename Vec<T>::type;
@@ -51,6 +52,19 @@ __global__ void __launch_bounds__(kThreads) small_cluster_kernel(const T* __rest
   TFB_CHECK(C <= kSmallMaxCluster && int64_t(C) * G >= P && gridDim.x == static_cast<unsigned>(C));
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int gsz = static_cast<int>(P2 < G ? P2 : G);  // leaves of this CTA's subtree
+  // Preamble (leaves_kernel has the same): ask the L2 for this CTA's contiguous G leaves
+  // before the grid dependency resolves — a hint, no data enters the SM.
+  if constexpr (VEC) {
+    if (prefetch && t < (DOT ? 2 : 1)) {
+      const int64_t start = int64_t(c) * G * Lel;
+      int64_t bytes = (n - start < G * Lel ? n - start : G * Lel) * static_cast<int64_t>(sizeof(T));
+      bytes &= ~int64_t(15);
+      if (bytes > 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((t ? y : x) + start),
+                     "r"(static_cast<unsigned>(bytes))
+                     : "memory");
+    }
+  }
   // programmatic dependent of the previous kernel (no memory access before it retired),
   // and itself lets the next kernel of the stream become resident early
   asm volatile("griddepcontrol.wait;" ::: "memory");

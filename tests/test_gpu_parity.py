@@ -1003,3 +1003,41 @@ def test_rows_class_uniform_kernel_matches_emulator(tfb, oracle, cuda, dt):
         ev, ee = oracle.emulate_rows(2, Xh, Y2h)
         for r in range(rows):
             _same(got[r], (ev[r], ee[r]), (dt, cols, "y other class", r))
+
+@pytest.mark.gpu
+def test_prefetch_preamble_is_result_neutral(tfb, oracle, cuda):
+    """The L2 prefetch preamble of the leaves / single-cluster kernels (tf_set_prefetch: off,
+    automatic, 4 KiB .. 512 KiB per operand per CTA) never changes a bit: ragged sizes whose
+    last leaf is partial or not a multiple of 16 bytes, rows with a padded pitch, sums and
+    dots, back-to-back launches in one stream (the preamble runs while the previous call's
+    tree kernel retires), inputs ending exactly at the end of their allocation."""
+    from paper_1401_0248_b200 import _lib
+    L = _lib.lib()
+    assert L.tf_set_prefetch(-2) == _lib.TF_EINVAL_ARG and L.tf_set_prefetch(513) == _lib.TF_EINVAL_ARG
+    try:
+        for dt in (np.float32, np.float64):
+            for n in (1023, 4096, 100003, (1 << 18) + 5, 1 << 20, (3 << 20) + 1234):
+                xh = oracle.lcg_fill("mmix", n, 81, dt, True)
+                yh = oracle.lcg_fill("nr", n, 82, dt, True)
+                x, y = torch.from_numpy(xh).to(cuda), torch.from_numpy(yh).to(cuda)  # exact-size allocations
+                for dot in (False, True):
+                    want = oracle.emulate(2, xh, yh if dot else None)
+                    for kb in (0, -1, 4, 32, 512):
+                        assert L.tf_set_prefetch(kb) == 0
+                        outs = [tfb.reduce(tfb.Method.TWOFOLD_FAST, x, y if dot else None) for _ in range(3)]
+                        for o in outs:
+                            _same(o.cpu().numpy(), want, (dt, n, dot, kb))
+        rows, cols, ld = 7, 70001, 70016
+        mh = oracle.lcg_fill("mmix", rows * ld, 83, np.float32, True).reshape(rows, ld)
+        m = torch.from_numpy(mh).to(cuda)
+        ev, ee = oracle.emulate_rows(3, mh[:, :cols], mh[:, :cols])
+        for kb in (0, -1, 64, 512):
+            L.tf_set_prefetch(kb)
+            got = tfb.reduce_rows(tfb.Method.TWOFOLD_RIGOROUS, m[:, :cols], m[:, :cols]).cpu().numpy()
+            for r in range(rows):
+                _same(got[r], (ev[r], ee[r]), ("rows", kb, r))
+    finally:
+        L.tf_set_prefetch(-1)
+
+
+
