@@ -472,6 +472,9 @@ __device__ __noinline__ void prefetch_first_leaf(const T* x, const T* y, int64_t
   if (off < bytes && (DOT || op == 0)) {
     const char* p = reinterpret_cast<const char*>((op ? y + r * ldy : x + r * ldx) + start) + off;
     const unsigned sz = static_cast<unsigned>(bytes - off < 4096 ? bytes - off : 4096);
+    // inside the row's leaf, 16-byte aligned and sized (the bulk prefetch's contract)
+    TFB_CHECK((reinterpret_cast<uintptr_t>(p) & 15u) == 0 && sz > 0 && (sz & 15u) == 0 &&
+              start + (off + sz) / static_cast<int64_t>(sizeof(T)) <= cols);
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(sz) : "memory");
   }
 }

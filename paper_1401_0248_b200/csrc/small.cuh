@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kThreads) small_cluster_kernel(const T* __rest
       const int64_t start = int64_t(c) * G * Lel;
       int64_t bytes = (n - start < G * Lel ? n - start : G * Lel) * static_cast<int64_t>(sizeof(T));
       bytes &= ~int64_t(15);
+      TFB_CHECK(bytes <= 0 || (reinterpret_cast<uintptr_t>((t ? y : x) + start) & 15u) == 0);
       if (bytes > 0)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((t ? y : x) + start),
                      "r"(static_cast<unsigned>(bytes))
