@@ -301,9 +301,12 @@ def sharded_reduce(method: Method, x_local: torch.Tensor, y_local: torch.Tensor 
         gathered = torch.empty((world, 2), dtype=local.dtype, device=local.device)
         dist.all_gather_into_tensor(gathered, local, group=group)
     else:
-        parts = [torch.empty_like(local) for _ in range(world)]
-        dist.all_gather(parts, local, group=group)
-        gathered = torch.stack(parts, 0)
+        # any other backend (gloo: CPU tensors only): the 8/16-byte pairs travel through host
+        # memory and the merge runs where the shards live
+        send = local.cpu() if local.is_cuda else local
+        parts = [torch.empty_like(send) for _ in range(world)]
+        dist.all_gather(parts, send, group=group)
+        gathered = torch.stack(parts, 0).to(local.device)
     return (merge or _default_merge)(method, gathered)
 
 
@@ -365,8 +368,10 @@ def sharded_rows(method: Method, X_local, Y_local=None, *, rows_global: int, lea
         dist.all_gather_into_tensor(table, padded, group=group)
         parts = list(table.split(block))
     else:
-        parts = [torch.empty_like(padded) for _ in range(world)]
-        dist.all_gather(parts, padded, group=group)
+        send = padded.cpu() if padded.is_cuda else padded  # gloo: through host memory
+        parts = [torch.empty_like(send) for _ in range(world)]
+        dist.all_gather(parts, send, group=group)
+        parts = [p.to(padded.device) for p in parts]
     return torch.cat([parts[r][: rows_range(rows_global, r, world)[1] - rows_range(rows_global, r, world)[0]]
                       for r in range(world)], 0)
 
