@@ -889,9 +889,28 @@ static int launch_leaves_tma(const T* px, const T* py, int64_t ldx, int64_t ldy,
            "leaves_tma_kernel<%s,%s,%s,NS=%d,SR=%d> grid=%u block=%d smem=%zu units=%lld leaf_log2=%d",
            method_tag(M), sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", NS, SR, grid, kTmaThreads, smem,
            static_cast<long long>(units), leaf_log2);
-  kern<<<grid, kTmaThreads, smem, stream>>>(px, py, ldx, ldy, rows, cols, leaf_log2, P,
-                                            static_cast<Pair<A>*>(partials), static_cast<unsigned*>(counters),
-                                            static_cast<Pair<A>*>(out), peer, epoch);
+  // programmatic dependent of the previous kernel + L2 prefetch preamble, like the LDG
+  // leaves kernel (launch_leaves_nt); the fused peer combine keeps the plain launch
+  static const bool chain_env = !getenv("TFB_PDL_CHAIN") || atoi(getenv("TFB_PDL_CHAIN")) != 0;
+  static const bool tma_chain = !getenv("TFB_TMA_CHAIN") || atoi(getenv("TFB_TMA_CHAIN")) != 0;
+  // (one-CTA-per-SM rings only: with the 3 / 4 CTA small rings it measured mixed, profiles/r02_tma_chain.txt)
+  const bool chain = chain_env && tma_chain && peer == nullptr && MINB == 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTmaThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = chain ? 1 : 0;
+  const int chain_pf_kb =
+      chain ? prefetch_kb_for(grid, DOT ? 2 : 1, rows * cols * int64_t(sizeof(T)) * (DOT ? 2 : 1)) : -1;
+  if (cudaLaunchKernelEx(&cfg, kern, px, py, ldx, ldy, rows, cols, leaf_log2, P, static_cast<Pair<A>*>(partials),
+                         static_cast<unsigned*>(counters), static_cast<Pair<A>*>(out), peer, epoch,
+                         chain_pf_kb) != cudaSuccess)
+    return record_cuda_error();
   return check_launch();
 }
 

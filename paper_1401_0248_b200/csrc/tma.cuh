@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) leaves_tma_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy, int64_t rows,
     int64_t cols, int leaf_log2, int64_t P, Pair<typename Acc<M, T>::type>* __restrict__ partials,
     unsigned* __restrict__ counters, Pair<typename Acc<M, T>::type>* __restrict__ out,
-    const PeerCtx* __restrict__ peer, uint32_t epoch) {
+    const PeerCtx* __restrict__ peer, uint32_t epoch, int chain_pf_kb) {
   using A = typename Acc<M, T>::type;
   using VT = typename Vec<T>::type;
   using L = TmaSmem<T, DOT, NS, SR>;
@@ -83,6 +83,26 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) leaves_tma_kernel(
   const int64_t units = rows * P;
   const int warp = threadIdx.x >> 5;
 
+  // Cross-call overlap (chain_pf_kb >= 0: launched as a programmatic dependent): a CTA of
+  // this grid becomes resident as soon as a CTA of the previous kernel frees its shared
+  // memory, asks the L2 for the head of its first leaf (a hint, leaves_kernel's preamble),
+  // and only then waits for the previous grid to complete — before any memory access.
+  if (chain_pf_kb >= 0) {
+    if (chain_pf_kb > 0 && threadIdx.x < 64 && static_cast<int64_t>(blockIdx.x) < units) {
+      const int64_t r = blockIdx.x / P;
+      const int64_t start = (blockIdx.x - r * P) * Lelems;
+      int64_t bytes = (cols - start < Lelems ? cols - start : Lelems) * static_cast<int64_t>(sizeof(T));
+      if (bytes > (static_cast<int64_t>(chain_pf_kb) << 10)) bytes = static_cast<int64_t>(chain_pf_kb) << 10;
+      bytes &= ~int64_t(15);
+      const int op = threadIdx.x & 1;
+      const int64_t off = static_cast<int64_t>(threadIdx.x >> 1) * 16384;
+      if (off < bytes && (DOT || op == 0)) {
+        const char* p = reinterpret_cast<const char*>((op ? y + r * ldy : x + r * ldx) + start) + off;
+        const unsigned sz = static_cast<unsigned>(bytes - off < 16384 ? bytes - off : 16384);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(sz) : "memory");
+      }
+    }
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < NS; ++i) {
       mbar_init(&full[i], 1);
@@ -91,6 +111,11 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) leaves_tma_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (chain_pf_kb >= 0) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // the next kernel of the stream may take this grid's SMs as its CTAs retire
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
 
   if (warp == kWarps) {  // ---------------- producer warp ----------------
     if ((threadIdx.x & 31) != 0) return;
