@@ -982,6 +982,26 @@ static int rows_kernel_choice() {
   return g_rows_kernel;
 }
 
+// The short-row kernels as programmatic dependents of the previous kernel in the stream
+// (wait before any memory access, L2 prefetch of each warp's first rows before the wait);
+// TFB_PDL_CHAIN=0 / TFB_ROWS_CHAIN=0 launch them plainly.  The kernels take the flag last.
+template <typename Kern, typename... Args>
+static int launch_rows_chained(Kern kern, unsigned grid, int block, cudaStream_t stream, Args... args) {
+  static const bool chain = (!getenv("TFB_PDL_CHAIN") || atoi(getenv("TFB_PDL_CHAIN")) != 0) &&
+                            (!getenv("TFB_ROWS_CHAIN") || atoi(getenv("TFB_ROWS_CHAIN")) != 0);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = chain ? 1 : 0;
+  if (cudaLaunchKernelEx(&cfg, kern, args..., chain ? 1 : 0) != cudaSuccess) return record_cuda_error();
+  return check_launch();
+}
+
 template <int M, typename T, bool DOT, int VEC>
 static int launch_rows_short(const T* px, const T* py, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
                              int leaf_log2, void* out, cudaStream_t stream) {
@@ -1002,9 +1022,8 @@ static int launch_rows_short(const T* px, const T* py, int64_t ldx, int64_t ldy,
            method_tag(M), sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum",
            VEC == 2 ? "ldg256" : VEC == 1 ? "ldg128" : "scalar", grid, kBlock, static_cast<long long>(rows),
            static_cast<long long>(cols), 1 << g_log2, leaf_log2);
-  kern<<<grid, kBlock, 0, stream>>>(px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2,
-                                      static_cast<Pair<A>*>(out));
-  return check_launch();
+  return launch_rows_chained(kern, grid, kBlock, stream, px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2,
+                             static_cast<Pair<A>*>(out));
 }
 
 // Misaligned one-leaf rows whose x / y share the 32-byte class sequence: class-uniform
@@ -1036,9 +1055,8 @@ static int launch_rows_cls(const T* px, const T* py, int64_t ldx, int64_t ldy, i
            "rows_cls_kernel<%s,%s,%s,win32> grid=%u block=%d rows=%lld cols=%lld lanes/row=%d period=%d leaf_log2=%d",
            method_tag(M), sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", grid, kBlock,
            static_cast<long long>(rows), static_cast<long long>(cols), 1 << g_log2, period, leaf_log2);
-  kern<<<grid, kBlock, 0, stream>>>(px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2, period,
-                                      static_cast<Pair<A>*>(out));
-  return check_launch();
+  return launch_rows_chained(kern, grid, kBlock, stream, px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2,
+                             period, static_cast<Pair<A>*>(out));
 }
 
 template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1, int MS = 0>

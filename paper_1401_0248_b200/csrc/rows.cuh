@@ -88,6 +88,21 @@ __device__ __forceinline__ void window32(const T* p, int m, int64_t rem, typenam
   for (int w = 0; w < 5; ++w) out[w] = mv ? c[w + 1] : c[w];
 }
 
+// Cross-call preamble of the short-row kernels (launched as programmatic dependents, like
+// leaves_kernel): lane 0 of every warp asks the L2 for the contiguous span of the warp's
+// first rows [p, p + bytes) — trimmed to whole 16-byte units inside the span, a hint only —
+// then the CTA waits for the previous grid before any memory access.
+__device__ __forceinline__ void prefetch_span(const void* p, int64_t bytes) {
+  const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + 15u) & ~uintptr_t(15);
+  int64_t n = bytes - static_cast<int64_t>(a - reinterpret_cast<uintptr_t>(p));
+  n &= ~int64_t(15);
+  if (n > 65536) n = 65536;
+  if (n > 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const void*>(a)),
+                 "r"(static_cast<unsigned>(n))
+                 : "memory");
+}
+
 // One 16-byte vector through a chain (elements in order).
 template <int M, typename T, bool DOT>
 __device__ __forceinline__ void chain_vec(Pair<typename Acc<M, T>::type>& st, const typename Vec<T>::type& a,
@@ -115,7 +130,7 @@ __device__ __forceinline__ T pick_at(const T (&flat)[N], int m, int i) {
 template <int M, typename T, bool DOT, int VEC>
 __global__ void TFB_RS_BOUNDS rows_short_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
-    int K, int g_log2, Pair<typename Acc<M, T>::type>* __restrict__ out) {
+    int K, int g_log2, Pair<typename Acc<M, T>::type>* __restrict__ out, int chain) {
   using A = typename Acc<M, T>::type;
   using VT = typename Vec<T>::type;
   constexpr int V = Vec<T>::V;
@@ -126,6 +141,16 @@ __global__ void TFB_RS_BOUNDS rows_short_kernel(
   const int64_t groups = 32 >> g_log2;
   const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  if (chain) {
+    const int64_t rf = warp * groups;
+    if (lane == 0 && rf < rows) {
+      const int64_t nr = rows - rf < groups ? rows - rf : groups;  // the warp's first rows: one contiguous span
+      prefetch_span(x + rf * ldx, ((nr - 1) * ldx + cols) * static_cast<int64_t>(sizeof(T)));
+      if constexpr (DOT) prefetch_span(y + rf * ldy, ((nr - 1) * ldy + cols) * static_cast<int64_t>(sizeof(T)));
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   // the loop bound is warp-uniform: every lane reaches every shuffle
   for (int64_t r0 = warp * groups; r0 < rows; r0 += nwarps * groups) {
     const int64_t r = r0 + (lane >> g_log2);
@@ -386,7 +411,7 @@ __device__ __forceinline__ void cls_rows_chains(Pair<typename Acc<M, T>::type> (
 template <int M, typename T, bool DOT>
 __global__ void TFB_RS_BOUNDS rows_cls_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
-    int K, int g_log2, int period, Pair<typename Acc<M, T>::type>* __restrict__ out) {
+    int K, int g_log2, int period, Pair<typename Acc<M, T>::type>* __restrict__ out, int chain) {
   using A = typename Acc<M, T>::type;
   constexpr int kChains = 8;
   constexpr int W = 32 / sizeof(T);
@@ -396,6 +421,16 @@ __global__ void TFB_RS_BOUNDS rows_cls_kernel(
   const int64_t groups = 32 >> g_log2;
   const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  if (chain) {
+    // the warp's first rows are `period` apart: one request per row, by the row group's first lane
+    const int64_t rf = (warp / period) * period * groups + warp % period + int64_t(period) * (lane >> g_log2);
+    if (j == 0 && rf < rows) {
+      prefetch_span(x + rf * ldx, cols * static_cast<int64_t>(sizeof(T)));
+      if constexpr (DOT) prefetch_span(y + rf * ldy, cols * static_cast<int64_t>(sizeof(T)));
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
   // slot s = (super-block s / p, class s % p); the warp's rows: q + p*i of the block
   for (int64_t s = warp;; s += nwarps) {  // warp-uniform
     const int64_t sb = s / period, q = s % period;
