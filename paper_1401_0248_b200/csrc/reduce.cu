@@ -986,9 +986,21 @@ static int rows_kernel_choice() {
 // (wait before any memory access, L2 prefetch of each warp's first rows before the wait);
 // TFB_PDL_CHAIN=0 / TFB_ROWS_CHAIN=0 launch them plainly.  The kernels take the flag last.
 template <typename Kern, typename... Args>
-static int launch_rows_chained(Kern kern, unsigned grid, int block, cudaStream_t stream, Args... args) {
+static int launch_rows_chained(Kern kern, unsigned grid, int block, cudaStream_t stream, int64_t input_bytes,
+                               int operands, Args... args) {
   static const bool chain = (!getenv("TFB_PDL_CHAIN") || atoi(getenv("TFB_PDL_CHAIN")) != 0) &&
                             (!getenv("TFB_ROWS_CHAIN") || atoi(getenv("TFB_ROWS_CHAIN")) != 0);
+  // bytes per warp and operand: the leaves kernels' budget (whole input up to 8 MiB, else
+  // 0.3 x input, at most 32 MiB) shared by the grid's warps
+  // measured (profiles/r02_rows_chain.txt): small calls gain 15-20 % (1000 x 64 f32 dot 2.74 -> 2.28 us,
+  // 4096 x 256: 3.67 -> 3.00), 32-64 MiB calls lose 2-6 %, large ones are level: chained up to 8 MiB
+  const bool use = chain && input_bytes <= (int64_t(8) << 20);
+  int pf = -1;
+  if (use) {
+    const int kb = prefetch_kb_for(grid, operands, input_bytes);  // KiB per CTA and operand
+    const int64_t per_warp = (static_cast<int64_t>(kb) << 10) / (block / 32);
+    pf = static_cast<int>(per_warp > 65536 ? 65536 : per_warp);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -997,8 +1009,8 @@ static int launch_rows_chained(Kern kern, unsigned grid, int block, cudaStream_t
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = chain ? 1 : 0;
-  if (cudaLaunchKernelEx(&cfg, kern, args..., chain ? 1 : 0) != cudaSuccess) return record_cuda_error();
+  cfg.numAttrs = use ? 1 : 0;
+  if (cudaLaunchKernelEx(&cfg, kern, args..., pf) != cudaSuccess) return record_cuda_error();
   return check_launch();
 }
 
@@ -1022,8 +1034,8 @@ static int launch_rows_short(const T* px, const T* py, int64_t ldx, int64_t ldy,
            method_tag(M), sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum",
            VEC == 2 ? "ldg256" : VEC == 1 ? "ldg128" : "scalar", grid, kBlock, static_cast<long long>(rows),
            static_cast<long long>(cols), 1 << g_log2, leaf_log2);
-  return launch_rows_chained(kern, grid, kBlock, stream, px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2,
-                             static_cast<Pair<A>*>(out));
+  return launch_rows_chained(kern, grid, kBlock, stream, rows * cols * int64_t(sizeof(T)) * (DOT ? 2 : 1), DOT ? 2 : 1,
+                             px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2, static_cast<Pair<A>*>(out));
 }
 
 // Misaligned one-leaf rows whose x / y share the 32-byte class sequence: class-uniform
@@ -1055,8 +1067,9 @@ static int launch_rows_cls(const T* px, const T* py, int64_t ldx, int64_t ldy, i
            "rows_cls_kernel<%s,%s,%s,win32> grid=%u block=%d rows=%lld cols=%lld lanes/row=%d period=%d leaf_log2=%d",
            method_tag(M), sizeof(T) == 4 ? "f32" : "f64", DOT ? "dot" : "sum", grid, kBlock,
            static_cast<long long>(rows), static_cast<long long>(cols), 1 << g_log2, period, leaf_log2);
-  return launch_rows_chained(kern, grid, kBlock, stream, px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2,
-                             period, static_cast<Pair<A>*>(out));
+  return launch_rows_chained(kern, grid, kBlock, stream, rows * cols * int64_t(sizeof(T)) * (DOT ? 2 : 1), DOT ? 2 : 1,
+                             px, py, ldx, ldy, rows, cols, static_cast<int>(K), g_log2, period,
+                             static_cast<Pair<A>*>(out));
 }
 
 template <int M, typename T, bool DOT, bool VEC, int NT, int UF = 1, int MS = 0>

@@ -92,11 +92,11 @@ __device__ __forceinline__ void window32(const T* p, int m, int64_t rem, typenam
 // leaves_kernel): lane 0 of every warp asks the L2 for the contiguous span of the warp's
 // first rows [p, p + bytes) — trimmed to whole 16-byte units inside the span, a hint only —
 // then the CTA waits for the previous grid before any memory access.
-__device__ __forceinline__ void prefetch_span(const void* p, int64_t bytes) {
+__device__ __forceinline__ void prefetch_span(const void* p, int64_t bytes, int cap) {
   const uintptr_t a = (reinterpret_cast<uintptr_t>(p) + 15u) & ~uintptr_t(15);
   int64_t n = bytes - static_cast<int64_t>(a - reinterpret_cast<uintptr_t>(p));
+  if (n > cap) n = cap;
   n &= ~int64_t(15);
-  if (n > 65536) n = 65536;
   if (n > 0)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const void*>(a)),
                  "r"(static_cast<unsigned>(n))
@@ -130,7 +130,7 @@ __device__ __forceinline__ T pick_at(const T (&flat)[N], int m, int i) {
 template <int M, typename T, bool DOT, int VEC>
 __global__ void TFB_RS_BOUNDS rows_short_kernel(
     const T* __restrict__ x, const T* __restrict__ y, int64_t ldx, int64_t ldy, int64_t rows, int64_t cols,
-    int K, int g_log2, Pair<typename Acc<M, T>::type>* __restrict__ out, int chain) {
+    int K, int g_log2, Pair<typename Acc<M, T>::type>* __restrict__ out, int chain) {  // chain: -1 plain launch, else bytes per warp and operand to prefetch
   using A = typename Acc<M, T>::type;
   using VT = typename Vec<T>::type;
   constexpr int V = Vec<T>::V;
@@ -141,12 +141,12 @@ __global__ void TFB_RS_BOUNDS rows_short_kernel(
   const int64_t groups = 32 >> g_log2;
   const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  if (chain) {
+  if (chain >= 0) {
     const int64_t rf = warp * groups;
-    if (lane == 0 && rf < rows) {
+    if (chain > 0 && lane == 0 && rf < rows) {
       const int64_t nr = rows - rf < groups ? rows - rf : groups;  // the warp's first rows: one contiguous span
-      prefetch_span(x + rf * ldx, ((nr - 1) * ldx + cols) * static_cast<int64_t>(sizeof(T)));
-      if constexpr (DOT) prefetch_span(y + rf * ldy, ((nr - 1) * ldy + cols) * static_cast<int64_t>(sizeof(T)));
+      prefetch_span(x + rf * ldx, ((nr - 1) * ldx + cols) * static_cast<int64_t>(sizeof(T)), chain);
+      if constexpr (DOT) prefetch_span(y + rf * ldy, ((nr - 1) * ldy + cols) * static_cast<int64_t>(sizeof(T)), chain);
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -421,12 +421,13 @@ __global__ void TFB_RS_BOUNDS rows_cls_kernel(
   const int64_t groups = 32 >> g_log2;
   const int64_t warp = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  if (chain) {
+  if (chain >= 0) {
     // the warp's first rows are `period` apart: one request per row, by the row group's first lane
     const int64_t rf = (warp / period) * period * groups + warp % period + int64_t(period) * (lane >> g_log2);
-    if (j == 0 && rf < rows) {
-      prefetch_span(x + rf * ldx, cols * static_cast<int64_t>(sizeof(T)));
-      if constexpr (DOT) prefetch_span(y + rf * ldy, cols * static_cast<int64_t>(sizeof(T)));
+    if (chain > 0 && j == 0 && rf < rows) {
+      const int cap = chain / static_cast<int>(groups) > 16 ? chain / static_cast<int>(groups) : 16;
+      prefetch_span(x + rf * ldx, cols * static_cast<int64_t>(sizeof(T)), cap);
+      if constexpr (DOT) prefetch_span(y + rf * ldy, cols * static_cast<int64_t>(sizeof(T)), cap);
     }
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
