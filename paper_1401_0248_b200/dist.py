@@ -318,9 +318,19 @@ def sharded_run(method: Method, x_local, y_local=None, *, n_global: int, leaf_lo
         x_local = torch.as_tensor(x_local)
     if y_local is not None and not isinstance(y_local, torch.Tensor):
         y_local = torch.as_tensor(y_local)
-    pair = sharded_reduce(method, x_local, y_local, n_global=n_global, leaf_log2=leaf_log2, group=group,
-                          local_reduce=local_reduce, merge=merge, track_product=track_product)
-    v, e = pair.cpu().tolist()
+    if (local_reduce is None and merge is None and not x_local.is_cuda and (y_local is None or not y_local.is_cuda)
+            and _world(group)[1] == 1):
+        # one rank, host-resident shard: the host-buffer engine already returns the pair in
+        # host memory — no bounce through a device tensor (two small copies and a sync less)
+        from .api import _device_for, _host_pair
+        lg = leaf_log2 or leaf_log2_for(x_local.dtype, n_global)
+        dev = _device_for(x_local)
+        with torch.cuda.device(dev):
+            v, e = _host_pair(method, x_local, y_local, dev, lg, track_product).tolist()
+    else:
+        pair = sharded_reduce(method, x_local, y_local, n_global=n_global, leaf_log2=leaf_log2, group=group,
+                              local_reduce=local_reduce, merge=merge, track_product=track_product)
+        v, e = pair.cpu().tolist()
     t = np.float64 if method is Method.WIDE else _np_type(x_local.dtype)
     if method in _TWOFOLD_METHODS:
         return SumResult(Twofold(t(v), t(e)), n_global)
