@@ -111,11 +111,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) leaves_tma_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (chain_pf_kb >= 0) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    // the next kernel of the stream may take this grid's SMs as its CTAs retire
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  }
+  if (chain_pf_kb >= 0) asm volatile("griddepcontrol.wait;" ::: "memory");
 
   if (warp == kWarps) {  // ---------------- producer warp ----------------
     if ((threadIdx.x & 31) != 0) return;
@@ -140,6 +136,10 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) leaves_tma_kernel(
         if (++slot == NS) { slot = 0; phase ^= 1u; }
       }
     }
+    // This CTA has issued its last bulk copy: once every CTA has, the next kernel of the
+    // stream may become resident (a kernel that needs no shared memory could otherwise sit
+    // beside this grid from its start and run its prefetch preamble far too early).
+    if (chain_pf_kb >= 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     return;
   }
 
