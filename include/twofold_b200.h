@@ -109,7 +109,9 @@ int tf_set_leaf_split(int split);
  * the initial value. */
 int tf_set_tail(int tail);
 
-/* Tuning knob (process-wide): L2 prefetch preamble of the LDG leaves kernel.  The
+/* Tuning knob (process-wide): L2 prefetch preamble of the streaming kernels (the
+ * LDG leaves and single-cluster kernels, the one-CTA-per-SM TMA rings, the short-row
+ * kernels up to 8 MiB).  The
  * kernel is launched as a programmatic dependent of whatever precedes it in the
  * stream; before it waits for that kernel's completion each CTA asks the L2 (bulk
  * prefetch, a hint: nothing is read into the SM, and the L2 is the point of
