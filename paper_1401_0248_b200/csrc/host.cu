@@ -246,6 +246,10 @@ struct HostEngine {
   void* counters = nullptr;
   int64_t counters_len = 0;
   CopyPool* pool = nullptr;
+  // staging copies of the hybrid path's GPU share: a small pool (TFB_HYBRID_COPY_THREADS,
+  // default 3 incl. the caller) — the full pool's spinning workers take cores from the leaf
+  // workers (pageable 2^26 f64 dot 13.8 -> 8.2 ms, profiles/r02_pageable_threads.txt)
+  CopyPool* hpool = nullptr;
   LeafPool* leaf_pool = nullptr;   // hybrid host path workers (nullptr: GPU only)
   size_t hybrid_min_bytes = 0;     // per operand; smaller host inputs stay GPU-only
   void* hpairs = nullptr;          // pinned: leaf pairs the host workers computed
@@ -278,6 +282,7 @@ void release(HostEngine* g) {
   if (g->stream) cudaStreamDestroy(g->stream);
   if (g->cstream) cudaStreamDestroy(g->cstream);
   delete g->pool;
+  delete g->hpool;
   delete g->leaf_pool;
   if (g->hpairs) cudaFreeHost(g->hpairs);
   delete g;
@@ -339,7 +344,9 @@ constexpr size_t kZeroCopyMaxPinned = size_t(256) << 10;
 constexpr size_t kZeroCopyMaxPageable = size_t(128) << 10;
 
 // Stage `bytes` of operand k (0 = x, 1 = y) from host `src` into device slot b.
-int stage(HostEngine* g, cudaStream_t s, int b, int k, const char* src, size_t bytes, Mem kind, bool wait_slot) {
+int stage(HostEngine* g, cudaStream_t s, int b, int k, const char* src, size_t bytes, Mem kind, bool wait_slot,
+          CopyPool* pool = nullptr) {
+  if (!pool) pool = g->pool;
   char* d = g->dev[b] + k * g->chunk;
   if (kind == Mem::kPinned) return cu(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s));
   if (wait_slot) {
@@ -350,7 +357,7 @@ int stage(HostEngine* g, cudaStream_t s, int b, int k, const char* src, size_t b
   char* p = g->pin[b] + k * g->chunk;
   for (size_t off = 0; off < bytes; off += kPiece) {
     const size_t m = std::min(kPiece, bytes - off);
-    g->pool->copy(p + off, src + off, m);
+    pool->copy(p + off, src + off, m);
     int rc = cu(cudaMemcpyAsync(d + off, p + off, m, cudaMemcpyHostToDevice, s));
     if (rc) return rc;
   }
@@ -546,8 +553,8 @@ int hybrid_reduce(HostEngine* g, int method, int dtype, const char* cx, const ch
     }
     Range r("gpu chunk");
     const size_t bytes = static_cast<size_t>(hi - lo) * L * item;
-    if ((rc = stage(g, g->cstream, b, 0, cx + lo * L * item, bytes, kx, false))) break;
-    if (dot && (rc = stage(g, g->cstream, b, 1, cy + lo * L * item, bytes, ky, false))) break;
+    if ((rc = stage(g, g->cstream, b, 0, cx + lo * L * item, bytes, kx, false, g->hpool))) break;
+    if (dot && (rc = stage(g, g->cstream, b, 1, cy + lo * L * item, bytes, ky, false, g->hpool))) break;
     if ((rc = cu(cudaEventRecord(g->h2d_done[b], g->cstream)))) break;
     if ((rc = cu(cudaStreamWaitEvent(g->stream, g->h2d_done[b], 0)))) break;
     rc = tf_reduce_leaves(method, dtype, g->dev[b], dot ? g->dev[b] + g->chunk : nullptr, (hi - lo) * L, lg,
@@ -643,6 +650,11 @@ int tf_host_engine_create(int device, int threads, size_t chunk_bytes, void** en
     return rc;
   }
   g->pool = new tfb::CopyPool(threads - 1);
+  {
+    const char* e = getenv("TFB_HYBRID_COPY_THREADS");
+    const int hc = std::max(1, std::min(e ? atoi(e) : 3, threads));
+    g->hpool = new tfb::CopyPool(hc - 1);
+  }
   // hybrid host path: all cores but the caller's by default (TFB_HYBRID_THREADS,
   // 0 = GPU only), for host inputs >= TFB_HYBRID_MIN_MB (default 8) per operand
   {
