@@ -907,10 +907,12 @@ int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, con
     const int64_t nblocks = (rows + block - 1) / block;
     const auto* cx = static_cast<const char*>(hx);
     const auto* cy = static_cast<const char*>(hy);
+    tfb::CopyPool* cpool = g->pool;  // the hybrid path stages with its small pool (set below)
     auto stage_block = [&](int b, int k, const char* src, int64_t ld, int64_t r0, int64_t nr, tfb::Mem kind,
                            bool wait) -> int {
       const char* s0 = src + static_cast<size_t>(r0) * ld * item;
-      if (ld == cols) return tfb::stage(g, g->cstream, b, k, s0, static_cast<size_t>(nr) * row_bytes, kind, wait);
+      if (ld == cols)
+        return tfb::stage(g, g->cstream, b, k, s0, static_cast<size_t>(nr) * row_bytes, kind, wait, cpool);
       char* d = g->dev[b] + k * g->chunk;
       if (kind == tfb::Mem::kPinned)  // pitched DMA packs the rows
         return tfb::cu(cudaMemcpy2DAsync(d, row_bytes, s0, ld * item, row_bytes, nr, cudaMemcpyHostToDevice,
@@ -920,7 +922,7 @@ int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, con
         if (e) return e;
       }
       char* p = g->pin[b] + k * g->chunk;
-      for (int64_t r = 0; r < nr; ++r) g->pool->copy(p + r * row_bytes, s0 + static_cast<size_t>(r) * ld * item, row_bytes);
+      for (int64_t r = 0; r < nr; ++r) cpool->copy(p + r * row_bytes, s0 + static_cast<size_t>(r) * ld * item, row_bytes);
       return tfb::cu(cudaMemcpyAsync(d, p, static_cast<size_t>(nr) * row_bytes, cudaMemcpyHostToDevice, g->cstream));
     };
     // Hybrid (as tf_host_reduce): the GPU claims row blocks from the front, the
@@ -928,6 +930,7 @@ int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, con
     // reducer: the same leaves and row tree), straight into the mapped row pairs.
     const bool hybrid = tfb::hybrid_methods(g, method, dtype, lg) && rows >= 2 &&
                         static_cast<size_t>(rows) * row_bytes >= g->hybrid_min_bytes;
+    if (hybrid && g->hpool) cpool = g->hpool;
     std::mutex cm;
     int64_t front = 0, back = rows;  // GPU owns [0, front), host owns [back, rows)
     std::atomic<int> host_rc{0};
