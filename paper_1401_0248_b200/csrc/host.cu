@@ -539,11 +539,46 @@ int hybrid_reduce(HostEngine* g, int method, int dtype, const char* cx, const ch
   });
   // GPU side: chunks from the front; a chunk is claimed only when a staging slot
   // is free (host wait), so the device never runs ahead of the link
+  // While it waits for a staging slot the calling thread reduces single leaves from the back
+  // too (its core would otherwise idle; TFB_HYBRID_CALLER_WORKS=0: sleep on the event instead).
+  static const bool caller_works = !getenv("TFB_HYBRID_CALLER_WORKS") || atoi(getenv("TFB_HYBRID_CALLER_WORKS")) != 0;
+  auto wait_slot = [&](int b) -> int {
+    if (!caller_works) return cu(cudaEventSynchronize(g->k_done[b]));
+    const unsigned csr = _mm_getcsr();
+    _mm_setcsr(csr & ~0x8040u);  // FTZ / DAZ off, like the workers
+    int r = TF_OK;
+    for (;;) {
+      const cudaError_t q = cudaEventQuery(g->k_done[b]);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) {
+        r = cu(q);
+        break;
+      }
+      int64_t lo, hi;
+      {
+        std::lock_guard<std::mutex> lk(cm);
+        if (back <= front) {
+          lo = hi = 0;
+        } else {
+          hi = back;
+          lo = std::max(front, back - 1);
+          back = lo;
+        }
+      }
+      if (hi == lo) {  // nothing left to steal: sleep until the slot is free
+        r = cu(cudaEventSynchronize(g->k_done[b]));
+        break;
+      }
+      if (host_leaves(method, dtype, cx, cy, lg, lo, hi, hp + lo * pair_bytes) != 0) host_rc.store(-1);
+    }
+    _mm_setcsr(csr);
+    return r;
+  };
   int64_t c = 0;
   for (;; ++c) {
     int64_t lo, hi;
     const int b = static_cast<int>(c & 1);
-    if (c >= 2 && (rc = cu(cudaEventSynchronize(g->k_done[b])))) break;
+    if (c >= 2 && (rc = wait_slot(b))) break;
     {
       std::lock_guard<std::mutex> lk(cm);
       if (front >= back) break;
