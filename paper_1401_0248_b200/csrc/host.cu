@@ -994,7 +994,44 @@ int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, con
     (void)nblocks;
     for (int64_t c = 0; rc == TF_OK; ++c) {
       const int b = static_cast<int>(c & 1);
-      if (hybrid && c >= 2 && (rc = tfb::cu(cudaEventSynchronize(g->k_done[b])))) break;
+      if (hybrid && c >= 2) {
+        // as in hybrid_reduce: the calling thread reduces whole rows from the back while it
+        // waits for the slot (rows of at most ~1 MiB at a time; TFB_HYBRID_CALLER_WORKS=0 sleeps)
+        static const bool caller_works =
+            !getenv("TFB_HYBRID_CALLER_WORKS") || atoi(getenv("TFB_HYBRID_CALLER_WORKS")) != 0;
+        if (!caller_works) {
+          if ((rc = tfb::cu(cudaEventSynchronize(g->k_done[b])))) break;
+        } else {
+          const int64_t cb = std::max<int64_t>(1, std::min<int64_t>(hb, (int64_t(1) << 20) / std::max<size_t>(row_bytes, 1)));
+          const unsigned csr = _mm_getcsr();
+          _mm_setcsr(csr & ~0x8040u);
+          for (;;) {
+            const cudaError_t q = cudaEventQuery(g->k_done[b]);
+            if (q == cudaSuccess) break;
+            if (q != cudaErrorNotReady) {
+              rc = tfb::cu(q);
+              break;
+            }
+            int64_t lo = 0, hi = 0;
+            {
+              std::lock_guard<std::mutex> lk(cm);
+              if (back > front) {
+                hi = back;
+                lo = std::max(front, back - cb);
+                back = lo;
+              }
+            }
+            if (hi == lo) {
+              rc = tfb::cu(cudaEventSynchronize(g->k_done[b]));
+              break;
+            }
+            if (tfb::host_rows(method, dtype, cx, cy, lo, hi, cols, ldx, ldy, lg, rp + lo * pair_bytes) != 0)
+              host_rc.store(-1);
+          }
+          _mm_setcsr(csr);
+          if (rc) break;
+        }
+      }
       int64_t r0, nr;
       {
         std::lock_guard<std::mutex> lk(cm);
