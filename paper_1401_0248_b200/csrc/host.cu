@@ -999,7 +999,7 @@ int tf_host_reduce_rows(void* engine, int method, int dtype, const void* hx, con
         // waits for the slot (rows of at most ~1 MiB at a time; TFB_HYBRID_CALLER_WORKS=0 sleeps)
         static const bool caller_works =
             !getenv("TFB_HYBRID_CALLER_WORKS") || atoi(getenv("TFB_HYBRID_CALLER_WORKS")) != 0;
-        if (!caller_works) {
+        if (!caller_works || row_bytes > (size_t(2) << 20)) {  // a long row would keep the caller from the GPU pipeline
           if ((rc = tfb::cu(cudaEventSynchronize(g->k_done[b])))) break;
         } else {
           const int64_t cb = std::max<int64_t>(1, std::min<int64_t>(hb, (int64_t(1) << 20) / std::max<size_t>(row_bytes, 1)));
